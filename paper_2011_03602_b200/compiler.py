@@ -1,0 +1,740 @@
+"""Per-app compiler: IR document -> host shared object + sm_100a cubin.
+
+The paper recompiles the program for every candidate pattern (PGI OpenACC,
+``PAPER.md:154``).  Here each program is compiled ONCE and every pattern of
+the GA becomes a runtime configuration:
+
+* every loop gets a CPU path (plain C, compiled with ``g++ -O3``, identical C
+  semantics to the reference's ``c_openacc`` rendering, ``src/codegen.py``);
+* every loop that can run on the GPU gets an sm_100a kernel plus a host launch
+  stub; a loop becomes a GPU root when the pattern says so
+  (``pattern.gpu_roots``, ``src/patterns.py:83-88``) and then takes its whole
+  subtree along (``src/patterns.py:76-82``);
+* every loop statement is a possible transfer site (a ``Placement`` always sits
+  at its anchor loop's statement, ``src/transfers.py:160-163``), so the
+  generated walk calls the runtime's hook before/after each loop whose site
+  carries directives in the current plan.
+
+Kernel shape (OpenACC ``kernels`` semantics): the maximal
+perfectly nested chain of parallelisable loops under the root (the
+reference's screen rules, ``src/screen.py:33-79``, restated in
+:func:`parallelizable`) is collapsed into a 1-D grid with the innermost loop
+fastest (coalesced along the contiguous index); the remaining loops run in
+order inside each thread.  Scalars read by the nest travel by value in the
+launch arguments; scalars written by the nest get lastprivate semantics (the
+thread owning the sequentially-last iteration stores them in a device slab).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import subprocess
+import tempfile
+import threading
+from dataclasses import dataclass
+from pathlib import Path
+
+from . import appspec
+from .ir import Program, expr_vars
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
+COMPILER_VERSION = "b2o-compiler-4"
+ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
+BLOCK_THREADS = 256
+
+_lock = threading.Lock()
+
+
+class CompileError(Exception):
+    """The program (or one of its variants) cannot be built for B200."""
+
+
+# ---------------------------------------------------------------------------
+# typing helpers
+# ---------------------------------------------------------------------------
+
+
+def ctype(prog: Program, vid: int, precision: str) -> str:
+    v = prog.vars[vid]
+    if v.base_type == "int":
+        return "int32_t"
+    return "float" if precision == "fp32" else "double"
+
+
+def etype(prog: Program, e, precision: str) -> str:
+    """C type of an expression under the usual arithmetic conversions."""
+    if e[0] == "num":
+        return "double" if e[2] else "int32_t"
+    if e[0] in ("var", "arr"):
+        return ctype(prog, e[1], precision)
+    a, b = etype(prog, e[2], precision), etype(prog, e[3], precision)
+    for t in ("double", "float"):
+        if t in (a, b):
+            return t
+    return "int32_t"
+
+
+def render(e, name) -> str:
+    """C text of an expression; ``name(vid, is_array)`` maps variables."""
+    k = e[0]
+    if k == "num":
+        v = e[1]
+        if e[2]:
+            s = repr(float(v))
+            return f"({s})" if float(v) < 0 else s
+        return f"({int(v)})" if int(v) < 0 else str(int(v))
+    if k == "var":
+        return name(e[1], False)
+    if k == "arr":
+        return f"{name(e[1], True)}[{render(e[2], name)}]"
+    return f"({render(e[2], name)} {e[1]} {render(e[3], name)})"
+
+
+# ---------------------------------------------------------------------------
+# nest analysis
+# ---------------------------------------------------------------------------
+
+
+def parallelizable(prog: Program, lid: int) -> bool:
+    """The reference's screen (src/screen.py:33-79), restated on the IR
+    document: no non-index scalar both read and set in the subtree, every array
+    write indexed by this loop's index variable, no impure call."""
+    loop = prog.loops[lid]
+    if prog.doc["loops"][lid].get("directive_error", False):
+        return False
+    regions = set(prog.subtree_regions(lid))
+    exempt = {prog.loops[x].index_var for x in prog.subtree_loops(lid)}
+    reads, sets = set(), set()
+    for o in prog.doc["occurrences"]:
+        if o["region"] not in regions or prog.vars[o["var"]].is_array or o["var"] in exempt:
+            continue
+        if o["kind"] == "read":
+            reads.add(o["var"])
+        elif o["kind"] == "set":
+            sets.add(o["var"])
+    if reads & sets:
+        return False
+    for st in prog.walk(loop.body):
+        if st.kind == "assign" and st.target[0] == "arr":
+            if loop.index_var not in expr_vars(st.target[2]):
+                return False
+        if st.kind == "call" and not prog.calls[st.call].pure:
+            return False
+        if st.kind == "replaced":
+            return False
+    return True
+
+
+@dataclass
+class NestPlan:
+    root: int
+    kernel: str | None
+    why_not: str | None
+    chain: list[int]
+    reads: list[int]        # vars whose value the nest needs (arrays: on device; scalars: by value)
+    writes: list[int]       # vars the nest writes
+    arrays: list[int]       # arrays referenced
+    scalar_args: list[int]  # scalars passed by value
+    swrites: list[int]      # scalars stored as lastprivate in the slab (incl. chain indices)
+    locals_: list[int]      # scalars living in thread-local registers (non-chain)
+
+
+def _first_access_is_read(prog: Program, lid: int, vid: int) -> bool:
+    """Walk the nest in execution order of one thread's first iteration; True
+    when ``vid`` may be read before any write (conservative)."""
+    def loop_first(l):
+        lo = prog.loops[l]
+        if vid in expr_vars(lo.lower):
+            return True
+        if lo.index_var == vid:
+            return False
+        if vid in expr_vars(lo.upper):
+            return True
+        return region_first(lo.body)
+
+    def region_first(rid):
+        for st in prog.regions[rid].statements:
+            if st.kind == "loop":
+                r = loop_first(st.loop)
+            elif st.kind == "call":
+                r = region_first(prog.calls[st.call].subtree) if not prog.is_opaque_call(st.call) else None
+            else:
+                reads, writes = prog.stmt_access(st)
+                if vid in reads:
+                    return True
+                r = False if vid in writes else None
+            if r is not None:
+                return r
+        return None
+
+    return bool(loop_first(lid))
+
+
+def plan_nest(prog: Program, lid: int) -> NestPlan:
+    loop = prog.loops[lid]
+    nest_loops = prog.subtree_loops(lid)
+    reads, writes = prog.subtree_access(lid)
+    why = None
+    for st in prog.walk(loop.body):
+        if st.kind == "replaced":
+            why = "subtree holds a replaced function block"
+        elif st.kind == "call" and prog.is_opaque_call(st.call):
+            why = f"subtree calls opaque {prog.calls[st.call].name!r}"
+    seen_idx = []
+    for x in nest_loops:
+        chain_up = [prog.loops[a].index_var for a in prog.ancestors(x) if a in nest_loops]
+        if prog.loops[x].index_var in chain_up:
+            why = why or "nested loops share an index variable"
+        seen_idx.append(prog.loops[x].index_var)
+    if why is not None:
+        return NestPlan(lid, None, why, [], [], [], [], [], [], [])
+    # assignments inside the nest (not loop headers)
+    body_writes = set()
+    for st in prog.walk(loop.body):
+        if st.kind in ("assign", "decl"):
+            body_writes |= prog.stmt_access(st)[1]
+    chain: list[int] = []
+    if parallelizable(prog, lid) and not (set(expr_vars(loop.lower)) | set(expr_vars(loop.upper))) & writes \
+            and loop.index_var not in body_writes:
+        chain = [lid]
+        while True:
+            body = prog.regions[prog.loops[chain[-1]].body].statements
+            if len(body) != 1 or body[0].kind != "loop":
+                break
+            c = body[0].loop
+            cl = prog.loops[c]
+            bound_vars = set(expr_vars(cl.lower)) | set(expr_vars(cl.upper))
+            chain_idx = {prog.loops[x].index_var for x in chain}
+            if (not parallelizable(prog, c) or bound_vars & (writes | chain_idx)
+                    or cl.index_var in chain_idx or cl.index_var in body_writes):
+                break
+            chain.append(c)
+    # chain bounds are evaluated on the host at launch: no arrays there
+    while chain and any(prog.vars[v].is_array for c in chain
+                        for v in expr_vars(prog.loops[c].lower) + expr_vars(prog.loops[c].upper)):
+        chain.pop()
+    chain_idx = [prog.loops[x].index_var for x in chain]
+    bound_scalars = {v for c in chain for v in expr_vars(prog.loops[c].lower) + expr_vars(prog.loops[c].upper)}
+    scalars = sorted(v for v in (reads | writes) if not prog.vars[v].is_array)
+    arrays = sorted(v for v in (reads | writes) if prog.vars[v].is_array)
+    locals_ = [v for v in scalars if v not in chain_idx]
+    scalar_args = [v for v in locals_ if v not in writes or _first_access_is_read(prog, lid, v)]
+    # roots evaluate chain bounds on the host: those reads are host-side
+    need = set(scalar_args) | {a for a in arrays if a in reads} | bound_scalars
+    swrites = sorted(set(chain_idx) | {v for v in locals_ if v in writes})
+    return NestPlan(lid, f"b2o_k{lid}", None, chain, sorted(need), sorted(writes), arrays,
+                    scalar_args, swrites, locals_)
+
+
+# ---------------------------------------------------------------------------
+# code generation
+# ---------------------------------------------------------------------------
+
+
+class _Gen:
+    def __init__(self, prog: Program, spec: dict):
+        self.prog = prog
+        self.spec = spec
+        self.precision = spec.get("precision", "fp32")
+        self.sets: list[tuple[tuple[int, ...], tuple[int, ...]]] = []
+        self.set_ids: dict = {}
+        self.blocks: list[dict] = []
+        self.block_ids: dict[int, int] = {}
+        self.calls: dict[int, dict] = {}
+        self.nests = {l.id: plan_nest(prog, l.id) for l in prog.loops}
+        self.device_op = {}
+        for l in prog.loops:
+            self.device_op[l.id] = any(st.kind == "replaced" for st in prog.walk(l.body))
+        for st in prog.stmts:
+            if st.kind == "replaced":
+                try:
+                    b = appspec.block_binding(prog, spec, st)
+                except ValueError as exc:
+                    raise CompileError(str(exc)) from exc
+                self.block_ids[st.uid] = len(self.blocks)
+                self.blocks.append(b)
+            elif st.kind == "call" and prog.is_opaque_call(st.call):
+                c = prog.calls[st.call]
+                try:
+                    b = appspec.external_call_binding(prog, spec, c)
+                except ValueError as exc:
+                    raise CompileError(str(exc)) from exc
+                for v in [b["out"]] + b["ins"]:
+                    if not prog.vars[v].is_array:
+                        raise CompileError(f"external {c.name!r} takes scalar argument {prog.vars[v].name!r}")
+                self.calls[c.id] = b
+        self.ext_writes = {cid: {b["out"]} for cid, b in self.calls.items()}
+
+    # -- helpers -----------------------------------------------------------
+
+    def T(self, vid: int) -> str:
+        return ctype(self.prog, vid, self.precision)
+
+    def access_set(self, reads, writes) -> int:
+        key = (tuple(sorted(set(reads) | set(writes))), tuple(sorted(writes)))
+        if key not in self.set_ids:
+            self.set_ids[key] = len(self.sets)
+            self.sets.append(key)
+        return self.set_ids[key]
+
+    def extra_writes(self, st):
+        if st.kind == "call" and st.call in self.ext_writes:
+            return self.ext_writes[st.call]
+        return set()
+
+    def subtree_access(self, lid):
+        return self.prog.subtree_access(lid, self.extra_writes)
+
+    @staticmethod
+    def host_name(vid: int, is_array: bool) -> str:
+        return f"A{vid}" if is_array else f"S{vid}"
+
+    @staticmethod
+    def local_name(vid: int, is_array: bool) -> str:
+        return f"v{vid}"
+
+    def bound(self, e, name) -> str:
+        t = etype(self.prog, e, self.precision)
+        txt = render(e, name)
+        if t == "int32_t":
+            return f"(int32_t)({txt})"
+        return f"(int32_t)ceil((double)({txt}))"
+
+    # -- CPU fast path -----------------------------------------------------------
+
+    def fast_fn(self, lid: int) -> list[str]:
+        prog = self.prog
+        reads, writes = self.subtree_access(lid)
+        used = sorted(reads | writes)
+        out = [f"static void fast_L{lid}(b2o_exec *ex) {{"]
+        for v in used:
+            t = self.T(v)
+            if prog.vars[v].is_array:
+                out.append(f"  {t} *__restrict__ v{v} = ({t} *)ex->host[{v}];")
+            else:
+                out.append(f"  {t} v{v} = *({t} *)ex->host[{v}];")
+        body: list[str] = []
+        self.fast_loop(lid, 1, body, outer=True)
+        out.extend(body)
+        out.append(f" out_L{lid}:")
+        for v in used:
+            if not prog.vars[v].is_array and v in writes:
+                out.append(f"  *({self.T(v)} *)ex->host[{v}] = v{v};")
+        for v in used:
+            if not prog.vars[v].is_array and v not in writes:
+                out.append(f"  (void)v{v};")
+        out.append("}")
+        return out
+
+    def fast_loop(self, lid: int, ind: int, out: list[str], outer: bool = False, label: int | None = None) -> None:
+        prog = self.prog
+        loop = prog.loops[lid]
+        label = lid if label is None else label
+        iv = f"v{loop.index_var}"
+        out.append("  " * ind + f"for ({iv} = {render(loop.lower, self.local_name)}; {iv} < "
+                   f"{render(loop.upper, self.local_name)}; {iv}++) {{")
+        if prog.children(lid):
+            out.append("  " * (ind + 1) + f"if (__builtin_expect(ex->stop, 0)) goto out_L{label};")
+        self.fast_region(loop.body, ind + 1, out, label)
+        out.append("  " * ind + "}")
+
+    def fast_region(self, rid: int, ind: int, out: list[str], label: int) -> None:
+        prog = self.prog
+        for st in prog.regions[rid].statements:
+            pad = "  " * ind
+            if st.kind == "decl":
+                if st.init is not None:
+                    out.append(pad + f"v{st.var} = {render(st.init, self.local_name)};")
+            elif st.kind == "assign":
+                out.append(pad + f"{render(st.target, self.local_name)} = {render(st.value, self.local_name)};")
+            elif st.kind == "loop":
+                self.fast_loop(st.loop, ind, out, label=label)
+            elif st.kind == "call":
+                if prog.is_opaque_call(st.call):
+                    out.append(pad + f"ex->external(ex, {st.call});")
+                    out.append(pad + f"if (ex->stop) goto out_L{label};")
+                else:
+                    self.fast_region(prog.calls[st.call].subtree, ind, out, label)
+            else:  # replaced blocks never reach the fast path
+                raise AssertionError("replaced block in a CPU fast path")
+
+    # -- instrumented walk ------------------------------------------------------
+
+    def instr_region(self, rid: int, ind: int, out: list[str]) -> None:
+        prog = self.prog
+        for st in prog.regions[rid].statements:
+            pad = "  " * ind
+            if st.kind in ("decl", "assign"):
+                reads, writes = prog.stmt_access(st)
+                if st.kind == "decl" and st.init is None:
+                    continue
+                sid = self.access_set(reads, writes)
+                out.append(pad + f"ex->host_access(ex, {sid}); if (ex->stop) return;")
+                if st.kind == "decl":
+                    out.append(pad + f"S{st.var} = {render(st.init, self.host_name)};")
+                else:
+                    out.append(pad + f"{render(st.target, self.host_name)} = {render(st.value, self.host_name)};")
+            elif st.kind == "loop":
+                self.instr_loop(st.loop, ind, out)
+            elif st.kind == "call":
+                if prog.is_opaque_call(st.call):
+                    out.append(pad + f"ex->external(ex, {st.call}); if (ex->stop) return;")
+                else:
+                    self.instr_region(prog.calls[st.call].subtree, ind, out)
+            else:
+                out.append(pad + f"ex->block(ex, {self.block_ids[st.uid]}); if (ex->stop) return;")
+
+    def instr_loop(self, lid: int, ind: int, out: list[str]) -> None:
+        prog = self.prog
+        loop = prog.loops[lid]
+        pad = "  " * ind
+        out.append(pad + f"if (ex->hook_mask[{lid}] & 1) {{ ex->hook(ex, {lid}, 0); if (ex->stop) return; }}")
+        branches = []
+        if self.nests[lid].kernel:
+            branches.append((f"ex->is_root[{lid}]", [f"launch_L{lid}(ex); if (ex->stop) return;"]))
+        if not self.device_op[lid]:
+            sid = self.access_set(*self.subtree_access(lid))
+            branches.append((f"!ex->dev_inside[{lid}]",
+                             [f"ex->host_access(ex, {sid}); if (ex->stop) return;",
+                              f"fast_L{lid}(ex); if (ex->stop) return;"]))
+        hr, hw = prog.loop_header_access(lid)
+        hsid = self.access_set(hr, hw)
+        iv = f"S{loop.index_var}"
+        inner = [f"ex->host_access(ex, {hsid}); if (ex->stop) return;",
+                 f"for ({iv} = {render(loop.lower, self.host_name)}; {iv} < {render(loop.upper, self.host_name)}; "
+                 f"{iv}++) {{"]
+        body: list[str] = []
+        self.instr_region(loop.body, 1, body)
+        inner.extend(body)
+        inner.append("}")
+        first = True
+        for cond, lines in branches:
+            out.append(pad + ("if (" if first else "} else if (") + cond + ") {")
+            out.extend(pad + "  " + ln for ln in lines)
+            first = False
+        if branches:
+            out.append(pad + "} else {")
+            out.extend(pad + "  " + ln for ln in inner)
+            out.append(pad + "}")
+        else:
+            out.extend(pad + ln for ln in inner)
+        out.append(pad + f"if (ex->hook_mask[{lid}] & 2) {{ ex->hook(ex, {lid}, 1); if (ex->stop) return; }}")
+
+    # -- kernels -------------------------------------------------------------------
+
+    def kernel_struct(self, n: NestPlan) -> list[str]:
+        D = max(len(n.chain), 1)
+        out = [f"typedef struct {{", "  uint32_t total;",
+               f"  uint32_t n[{D}], mul[{D}], shr[{D}];", f"  int32_t lo[{D}];", "  void *slab;"]
+        reads = set(n.reads)
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  {const}{self.T(v)} *p{v};")
+        for v in n.scalar_args:
+            out.append(f"  {self.T(v)} s{v};")
+        out.append(f"}} KA_L{n.root};")
+        del reads
+        return out
+
+    def launch_fn(self, n: NestPlan) -> list[str]:
+        prog = self.prog
+        lid = n.root
+        out = [f"static void launch_L{lid}(b2o_exec *ex) {{", f"  ex->pre_launch(ex, {lid}); if (ex->stop) return;",
+               f"  KA_L{lid} a; memset(&a, 0, sizeof a);", "  uint64_t total = 1;"]
+        for d, c in enumerate(n.chain):
+            cl = prog.loops[c]
+            out.append(f"  {{ int32_t lo = {self.bound(cl.lower, self.host_name)}; "
+                       f"int32_t hi = {self.bound(cl.upper, self.host_name)};")
+            out.append(f"    a.lo[{d}] = lo; a.n[{d}] = hi > lo ? (uint32_t)((int64_t)hi - lo) : 0u; "
+                       f"total *= a.n[{d}]; }}")
+        if n.chain:
+            out.append("  if (total == 0) {")
+            sid = self.access_set(*self.subtree_access(lid))
+            out.append(f"    ex->host_access(ex, {sid}); if (ex->stop) return;")
+            out.append(f"    fast_L{lid}(ex); return;")
+            out.append("  }")
+            out.append("  if (total > 0xFFFFFFFFull) { ex->launch(ex, %d, 0, 0, 0); return; }" % lid)
+            for d in range(1, len(n.chain)):
+                out.append(f"  b2o_fastdiv_init(a.n[{d}], &a.mul[{d}], &a.shr[{d}]);")
+        out.append("  a.total = (uint32_t)total; a.slab = ex->slab;")
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  a.p{v} = ({const}{self.T(v)} *)ex->dev[{v}];")
+        for v in n.scalar_args:
+            out.append(f"  a.s{v} = S{v};")
+        out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, a.total);")
+        out.append("}")
+        return out
+
+    def kernel_fn(self, n: NestPlan) -> list[str]:
+        prog = self.prog
+        lid = n.root
+        out = [f'extern "C" __global__ void __launch_bounds__({BLOCK_THREADS}) {n.kernel}(const KA_L{lid} a) {{']
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        out.append("  const uint32_t stride = gridDim.x * blockDim.x;")
+        out.append("  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {")
+        D = len(n.chain)
+        for c in n.chain:
+            out.append(f"    int32_t v{prog.loops[c].index_var}_;")
+        if D:
+            out.append("    uint32_t r = t;")
+            for d in range(D - 1, 0, -1):
+                iv = prog.loops[n.chain[d]].index_var
+                out.append(f"    {{ uint32_t q = b2o_fastdiv(r, a.mul[{d}], a.shr[{d}]); "
+                           f"v{iv}_ = a.lo[{d}] + (int32_t)(r - q * a.n[{d}]); r = q; }}")
+            out.append(f"    v{prog.loops[n.chain[0]].index_var}_ = a.lo[0] + (int32_t)r;")
+        for c in n.chain:
+            iv = prog.loops[c].index_var
+            out.append(f"    const int32_t v{iv} = v{iv}_;")
+        for v in n.locals_:
+            init = f"a.s{v}" if v in n.scalar_args else "0"
+            cq = "const " if v not in n.writes else ""
+            out.append(f"    {cq}{self.T(v)} v{v} = {init};")
+        body: list[str] = []
+        if D:
+            self.dev_region(prog.loops[n.chain[-1]].body, 2, body)
+        else:
+            self.dev_loop(lid, 2, body)
+        out.extend(body)
+        out.append("    if (t == a.total - 1u) {")
+        for v in n.swrites:
+            if v in [prog.loops[c].index_var for c in n.chain]:
+                d = [prog.loops[c].index_var for c in n.chain].index(v)
+                val = f"a.lo[{d}] + (int32_t)a.n[{d}]"
+            else:
+                val = f"v{v}"
+            out.append(f"      *({self.T(v)} *)((char *)a.slab + 8 * {v}) = {val};")
+        out.append("    }")
+        for v in n.locals_:
+            if v not in n.swrites:
+                out.append(f"    (void)v{v};")
+        out.append("  }")
+        out.append("}")
+        return out
+
+    def dev_loop(self, lid: int, ind: int, out: list[str]) -> None:
+        loop = self.prog.loops[lid]
+        iv = f"v{loop.index_var}"
+        out.append("  " * ind + f"for ({iv} = {render(loop.lower, self.local_name)}; {iv} < "
+                   f"{render(loop.upper, self.local_name)}; {iv}++) {{")
+        self.dev_region(loop.body, ind + 1, out)
+        out.append("  " * ind + "}")
+
+    def dev_region(self, rid: int, ind: int, out: list[str]) -> None:
+        prog = self.prog
+        for st in prog.regions[rid].statements:
+            pad = "  " * ind
+            if st.kind == "decl":
+                if st.init is not None:
+                    out.append(pad + f"v{st.var} = {render(st.init, self.local_name)};")
+            elif st.kind == "assign":
+                out.append(pad + f"{render(st.target, self.local_name)} = {render(st.value, self.local_name)};")
+            elif st.kind == "loop":
+                self.dev_loop(st.loop, ind, out)
+            elif st.kind == "call":
+                self.dev_region(prog.calls[st.call].subtree, ind, out)
+            else:
+                raise AssertionError("replaced block inside a kernel")
+
+    # -- module ------------------------------------------------------------------------
+
+    def generate(self) -> tuple[str, str, str]:
+        prog = self.prog
+        digest = prog.digest()
+        hdr = ["#pragma once", '#include "b2o_module.h"', "#include <stdint.h>"]
+        for n in self.nests.values():
+            if n.kernel:
+                hdr.extend(self.kernel_struct(n))
+        # device source
+        dev = ['#include "app.h"', ""]
+        for n in self.nests.values():
+            if n.kernel:
+                dev.extend(self.kernel_fn(n))
+                dev.append("")
+        # host source
+        host = ["#include <math.h>", "#include <string.h>", '#include "app.h"', ""]
+        for v in prog.vars:
+            t = self.T(v.id)
+            if v.is_array:
+                host.append(f"#define A{v.id} (({t} *)ex->host[{v.id}])  /* {v.name} */")
+            else:
+                host.append(f"#define S{v.id} (*({t} *)ex->host[{v.id}])  /* {v.name} */")
+        host.append("")
+        for l in prog.loops:
+            if not self.device_op[l.id]:
+                host.extend(self.fast_fn(l.id))
+        for n in self.nests.values():
+            if n.kernel:
+                host.extend(self.launch_fn(n))
+        run = ['extern "C" void b2o_mod_run(b2o_exec *ex) {']
+        self.instr_region(prog.root, 1, run)
+        run.append("}")
+        host.extend(run)
+        host.extend(self.info_tables(digest))
+        return "\n".join(hdr) + "\n", "\n".join(dev) + "\n", "\n".join(host) + "\n"
+
+    def info_tables(self, digest: str) -> list[str]:
+        prog = self.prog
+        elem = {"int32_t": 0, "float": 1, "double": 2}
+        written = set()
+        for st in prog.stmts:
+            written |= prog.stmt_access(st)[1]
+            if st.kind == "loop":
+                written.add(prog.loops[st.loop].index_var)
+        for b in list(self.blocks) + list(self.calls.values()):
+            written.add(b["out"])
+        out = []
+
+        def arr(name, ctype_, items):
+            body = ", ".join(str(x) for x in items) if items else "0"
+            n = max(len(items), 1)
+            out.append(f"static const {ctype_} {name}[{n}] = {{{body}}};")
+
+        def vs(prefix, vals):
+            arr(prefix, "int32_t", list(vals))
+            return f"{{{len(vals)}, {prefix}}}"
+
+        out.append("static const b2o_var_info VARS[] = {")
+        for v in prog.vars:
+            out.append(f'  {{"{v.name}", {int(v.is_array)}, {elem[self.T(v.id)]}, {v.length if v.is_array else 1}, '
+                       f"{int(v.id in written)}, 0}},")
+        out.append("};")
+        loop_rows = []
+        for l in prog.loops:
+            n = self.nests[l.id]
+            r = vs(f"LR{l.id}", n.reads)
+            w = vs(f"LW{l.id}", n.writes)
+            s = vs(f"LS{l.id}", n.swrites)
+            kern = f'"{n.kernel}"' if n.kernel else "0"
+            why = json.dumps(n.why_not) if n.why_not else "0"
+            parent = -1 if l.parent is None else l.parent
+            loop_rows.append(f"  {{{kern}, {parent}, {l.index_var}, {len(n.chain)}, {int(self.device_op[l.id])}, "
+                             f"{r}, {w}, {s}, {why}}},")
+        set_rows, wrow = [], []
+        for i, (allv, wv) in enumerate(self.sets):
+            set_rows.append("  " + vs(f"SA{i}", allv) + ",")
+            wrow.append("  " + vs(f"SW{i}", wv) + ",")
+        out.append("static const b2o_loop_info LOOPS[] = {")
+        out.extend(loop_rows or ["  {0}"])
+        out.append("};")
+        out.append("static const b2o_varset SETS[] = {")
+        out.extend(set_rows or ["  {0, 0}"])
+        out.append("};")
+        out.append("static const b2o_varset SETW[] = {")
+        out.extend(wrow or ["  {0, 0}"])
+        out.append("};")
+        outputs = appspec.outputs_of(prog, self.spec)
+        out.append("static const b2o_output_info OUTS[] = {")
+        for vid, rel, mode in outputs:
+            out.append(f"  {{{vid}, {1 if mode == 'normwise' else 0}, {rel!r}}},")
+        if not outputs:
+            out.append("  {0, 0, 0.0}")
+        out.append("};")
+
+        def op_row(b):
+            if b is None:
+                return "  {-1, 0, 0, 0, 0, 0, 0},"
+            op = 0 if b["kind"] == "gemm" else 1
+            ins = b["ins"] + [-1, -1]
+            return (f"  {{{op}, {b['out']}, {ins[0]}, {ins[1]}, {b.get('m', b.get('n', 0))}, "
+                    f"{b.get('n', 0)}, {b.get('k', 0)}}},")
+
+        out.append("static const b2o_op_info BLOCKS[] = {")
+        out.extend([op_row(b) for b in self.blocks] or ["  {-1, 0, 0, 0, 0, 0, 0}"])
+        out.append("};")
+        out.append("static const b2o_op_info CALLS[] = {")
+        out.extend([op_row(self.calls.get(c.id)) for c in prog.calls] or ["  {-1, 0, 0, 0, 0, 0, 0}"])
+        out.append("};")
+        prec = 1 if self.precision == "fp32" else 2
+        out.append("static const b2o_module_info INFO = {")
+        out.append(f"  B2O_MODULE_ABI, {len(prog.vars)}, {len(prog.loops)}, {len(self.sets)}, {len(outputs)}, "
+                   f"{len(self.blocks)}, {len(prog.calls)}, {prec},")
+        out.append(f'  VARS, LOOPS, SETS, SETW, OUTS, BLOCKS, CALLS, "{digest}"')
+        out.append("};")
+        out.append('extern "C" const b2o_module_info *b2o_mod_info(void) { return &INFO; }')
+        return out
+
+
+# ---------------------------------------------------------------------------
+# build + cache
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class CompiledApp:
+    key: str
+    host_so: Path
+    cubin: Path
+    source_dir: Path
+    nests: dict
+    n_loops: int
+
+
+def _spec_key(spec: dict) -> dict:
+    return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad")}
+
+
+def build_key(doc: dict, spec: dict) -> str:
+    blob = json.dumps({"doc": doc, "spec": _spec_key(spec), "v": COMPILER_VERSION}, sort_keys=True)
+    return hashlib.sha256(blob.encode()).hexdigest()[:24]
+
+
+def _run(cmd: list[str], cwd: Path) -> None:
+    p = subprocess.run(cmd, cwd=cwd, capture_output=True, text=True)
+    if p.returncode != 0:
+        raise CompileError(f"{cmd[0]} failed ({p.returncode}): {(p.stdout + p.stderr)[-1500:]}")
+
+
+def compile_program(doc: dict, spec: dict, cache_dir: Path | None = None) -> CompiledApp:
+    """Generate and build (or fetch from the cache) one program's module."""
+    prog = Program(doc)
+    gen = _Gen(prog, spec)
+    key = build_key(doc, spec)
+    cache = Path(cache_dir or CACHE)
+    out_dir = cache / key
+    host_so = out_dir / "app_host.so"
+    cubin = out_dir / "app.cubin"
+    nests = gen.nests
+    if host_so.exists() and cubin.exists():
+        return CompiledApp(key, host_so, cubin, out_dir, nests, len(prog.loops))
+    hdr, dev, host = gen.generate()
+    with _lock:
+        if host_so.exists() and cubin.exists():
+            return CompiledApp(key, host_so, cubin, out_dir, nests, len(prog.loops))
+        cache.mkdir(parents=True, exist_ok=True)
+        tmp = Path(tempfile.mkdtemp(prefix=f"{key}.", dir=cache))
+        (tmp / "app.h").write_text(hdr)
+        (tmp / "app_dev.cu").write_text(dev)
+        (tmp / "app_host.cpp").write_text(host)
+        inc = ["-I", str(CSRC), "-I", str(tmp)]
+        fmad = "true" if spec.get("fmad", True) else "false"
+        nvcc = os.environ.get("NVCC", "nvcc")
+        jobs = [
+            ["g++", "-O3", "-std=c++17", "-shared", "-fPIC", "-ffp-contract=off", "-fno-fast-math", *inc,
+             "app_host.cpp", "-o", "app_host.so"],
+            [nvcc, "-cubin", *ARCH_FLAGS, "-O3", "-lineinfo", f"-fmad={fmad}", "-std=c++17", *inc,
+             "app_dev.cu", "-o", "app.cubin"],
+        ]
+        procs = [subprocess.Popen(c, cwd=tmp, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+                 for c in jobs]
+        for c, p in zip(jobs, procs):
+            text, _ = p.communicate()
+            if p.returncode != 0:
+                raise CompileError(f"{c[0]} failed ({p.returncode}): {text[-2000:]}")
+        try:
+            os.replace(tmp, out_dir)
+        except OSError:
+            # another process won the race; keep theirs
+            pass
+    return CompiledApp(key, host_so, cubin, out_dir, nests, len(prog.loops))
+
+
+def generate_sources(doc: dict, spec: dict) -> tuple[str, str, str]:
+    """(app.h, app_dev.cu, app_host.cpp) without building; for inspection/tests."""
+    return _Gen(Program(doc), spec).generate()

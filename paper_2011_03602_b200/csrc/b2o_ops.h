@@ -1,0 +1,18 @@
+// Operations behind opaque library calls (CPU bindings, SURVEY.md Appendix
+// A.5) and behind the pattern-DB replacements cublas_gemm / cufft_exec
+// (hand-written sm_100a kernels; reference fixtures/sample_db.json:6,15).
+#pragma once
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+// host: C = A B, row-major m x k times k x n, double accumulation
+void b2o_cpu_gemm(const void *A, const void *B, void *C, int64_t m, int64_t n, int64_t k, int elem);
+// host: y = forward 2-D DFT of x (interleaved complex, n x n), double precision
+void b2o_cpu_fft2d(const void *x, void *y, int64_t n, int elem);
+
+#ifdef __cplusplus
+}
+#endif

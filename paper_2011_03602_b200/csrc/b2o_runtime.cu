@@ -1,0 +1,1025 @@
+// b2o_runtime.cu — pattern executor, device-resident variable manager and
+// worker pool behind include/b2o.h.
+//
+// One worker thread per B200 owns a CUDA stream and, for every loaded app, a
+// full replica of the app state (pinned host working copies, device buffers,
+// pristine copies for per-pattern reset).  A job is one candidate pattern:
+//
+//   reset (untimed) -> run the generated host walk (timed wall clock, all GPU
+//   work synchronised) -> fetch outputs -> compare against the reference
+//   outputs with the reference's rule (src/evaluators.py:129-139).
+//
+// The variable manager keeps, per variable, host-valid / device-valid bits.
+// Plan directives (src/transfers.py:45-53) execute at their placement hooks
+// (the anchor loop's statement, before/after); in COHERENT mode a directive
+// whose target copy is already valid is elided, and any access that would
+// read stale data triggers a counted "unplanned" transfer.
+// Scalars read by a kernel ride in the launch arguments (the H2D of a scalar
+// is satisfied by value); scalars written by a kernel land in a device slab.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/b2o.h"
+#include "b2o_module.h"
+#include "b2o_ops.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_mu;
+
+int fail(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return -1;
+}
+
+using Clock = std::chrono::steady_clock;
+
+size_t elem_bytes(int elem) { return elem == B2O_F64 ? 8 : 4; }
+
+struct AppShared;
+
+struct Worker {
+  int index = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::thread th;
+  bool broken = false;
+  std::string broken_why;
+  std::atomic<int64_t> deadline_ns{0};
+  std::atomic<b2o_exec *> running{nullptr};
+  std::atomic<int> timed_out{0};
+};
+
+// Per (app, worker) replica.
+struct AppDev {
+  AppShared *app = nullptr;
+  Worker *w = nullptr;
+  CUmodule mod = nullptr;
+  std::vector<CUfunction> kfun;
+  std::vector<void *> host, dev, dev_pristine;
+  void *cells = nullptr;     // pinned 8-byte scalar cells
+  void *slab = nullptr;      // device scalar slab
+  void *slab_init = nullptr; // pinned initial slab contents
+  std::vector<uint8_t> hv, dv, hmod, dev_dirty;
+  std::vector<uint8_t> is_root, dev_inside, hook_mask;
+  std::vector<std::vector<b2o_directive>> hooks[2];
+  b2o_exec ex{};
+  int mode = B2O_MODE_COHERENT;
+  b2o_result acc{};
+  int err_validity = B2O_VALID;
+  std::string err;
+  bool have_final = false;
+};
+
+struct AppShared {
+  std::string host_path, cubin_path;
+  void *dl = nullptr;
+  const b2o_module_info *info = nullptr;
+  b2o_mod_run_fn run = nullptr;
+  std::vector<char> image;
+  std::vector<std::vector<char>> initial;    // per var
+  std::map<int, std::vector<char>> reference;  // per output var
+  bool finalized = false;
+  double ref_time = -1.0;
+  std::vector<std::unique_ptr<AppDev>> per_worker;
+};
+
+struct Job {
+  AppShared *app;
+  b2o_pattern pat;
+  std::vector<uint8_t> roots;
+  std::vector<b2o_directive> dirs;
+  b2o_result res{};
+  struct Batch *batch;
+  size_t slot;
+};
+
+struct Batch {
+  std::vector<Job> jobs;
+  size_t remaining = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+};
+
+struct Runtime {
+  std::vector<std::unique_ptr<Worker>> workers;
+  std::deque<Job *> queue;
+  std::mutex qmu;
+  std::condition_variable qcv;
+  bool stopping = false;
+  std::thread watchdog;
+  std::map<uint64_t, std::unique_ptr<AppShared>> apps;
+  std::map<uint64_t, std::unique_ptr<Batch>> batches;
+  uint64_t next_id = 1;
+};
+
+Runtime *g_rt = nullptr;
+
+// Driver API through the runtime's entry-point query, so libb2o.so does not
+// link libcuda.so.1 and loads (for ABI checks) on machines without a driver.
+struct DriverApi {
+  decltype(&::cuModuleLoadData) moduleLoadData = nullptr;
+  decltype(&::cuModuleGetFunction) moduleGetFunction = nullptr;
+  decltype(&::cuModuleUnload) moduleUnload = nullptr;
+  decltype(&::cuLaunchKernel) launchKernel = nullptr;
+  decltype(&::cuGetErrorString) getErrorString = nullptr;
+} drv;
+
+template <typename F>
+bool driver_sym(const char *name, F *out) {
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return false;
+  *out = reinterpret_cast<F>(fn);
+  return true;
+}
+
+bool load_driver_api() {
+  return driver_sym("cuModuleLoadData", &drv.moduleLoadData) &&
+         driver_sym("cuModuleGetFunction", &drv.moduleGetFunction) &&
+         driver_sym("cuModuleUnload", &drv.moduleUnload) && driver_sym("cuLaunchKernel", &drv.launchKernel) &&
+         driver_sym("cuGetErrorString", &drv.getErrorString);
+}
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now().time_since_epoch()).count();
+}
+
+// ---------------------------------------------------------------------------
+// variable manager primitives (all on the worker's stream)
+// ---------------------------------------------------------------------------
+
+AppDev *D(b2o_exec *ex) { return static_cast<AppDev *>(ex->rt); }
+
+void set_error(AppDev *d, int validity, const std::string &msg) {
+  if (d->err_validity == B2O_VALID) {
+    d->err_validity = validity;
+    d->err = msg;
+  }
+  d->ex.stop = 1;
+}
+
+bool cuda_ok(AppDev *d, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return true;
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  if (e == cudaErrorIllegalAddress || e == cudaErrorLaunchFailure || e == cudaErrorIllegalInstruction ||
+      e == cudaErrorMisalignedAddress || e == cudaErrorHardwareStackError) {
+    d->w->broken = true;
+    d->w->broken_why = m;
+  }
+  set_error(d, B2O_RUNTIME_ERROR, m);
+  return false;
+}
+
+bool cu_ok(AppDev *d, CUresult r, const char *what) {
+  if (r == CUDA_SUCCESS) return true;
+  const char *s = nullptr;
+  drv.getErrorString(r, &s);
+  return cuda_ok(d, cudaErrorUnknown, (std::string(what) + ": " + (s ? s : "?")).c_str());
+}
+
+const b2o_var_info &VI(AppDev *d, int v) { return d->app->info->vars[v]; }
+
+size_t var_bytes(AppDev *d, int v) {
+  const b2o_var_info &vi = VI(d, v);
+  return vi.is_array ? (size_t)vi.length * elem_bytes(vi.elem) : elem_bytes(vi.elem);
+}
+
+void copy_h2d(AppDev *d, int v) {
+  cuda_ok(d, cudaMemcpyAsync(d->dev[v], d->host[v], var_bytes(d, v), cudaMemcpyHostToDevice, d->w->stream),
+          "H2D copy");
+  d->dev_dirty[v] = 1;
+}
+
+void copy_d2h(AppDev *d, int v) {
+  if (VI(d, v).is_array) {
+    cuda_ok(d, cudaMemcpyAsync(d->host[v], d->dev[v], var_bytes(d, v), cudaMemcpyDeviceToHost, d->w->stream),
+            "D2H copy");
+  } else {
+    cuda_ok(d, cudaMemcpyAsync(d->host[v], (char *)d->slab + 8 * v, var_bytes(d, v), cudaMemcpyDeviceToHost,
+                               d->w->stream),
+            "D2H scalar copy");
+  }
+  cuda_ok(d, cudaStreamSynchronize(d->w->stream), "D2H sync");
+}
+
+// make the host copy current (coherent mode)
+void ensure_host(AppDev *d, int v) {
+  if (d->hv[v]) return;
+  if (d->mode == B2O_MODE_LITERAL) {
+    d->acc.stale_reads++;
+    return;
+  }
+  copy_d2h(d, v);
+  d->acc.unplanned_bytes += var_bytes(d, v);
+  d->hv[v] = 1;
+}
+
+// make the device copy current (arrays)
+void ensure_dev(AppDev *d, int v, uint64_t *counter) {
+  if (d->dv[v]) return;
+  if (d->mode == B2O_MODE_LITERAL && counter == &d->acc.unplanned_bytes) {
+    d->acc.stale_reads++;
+    return;
+  }
+  copy_h2d(d, v);
+  *counter += var_bytes(d, v);
+  d->dv[v] = 1;
+}
+
+// an array about to be (fully or partially) overwritten on the device
+void prepare_dev_write(AppDev *d, int v, uint64_t *counter) {
+  if (d->dv[v]) return;
+  if (d->hmod[v]) {
+    ensure_dev(d, v, counter);
+  } else {
+    // never touched by the host since reset: the device buffer already holds
+    // the pristine contents (present-by-allocation, no copy needed)
+    d->dv[v] = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// callbacks used by generated code
+// ---------------------------------------------------------------------------
+
+void cb_host_access(b2o_exec *ex, int32_t set) {
+  AppDev *d = D(ex);
+  const b2o_varset &all = d->app->info->sets[set];
+  const b2o_varset &wr = d->app->info->set_writes[set];
+  for (int i = 0; i < all.n && !ex->stop; ++i) ensure_host(d, all.vars[i]);
+  for (int i = 0; i < wr.n; ++i) {
+    int v = wr.vars[i];
+    d->hv[v] = 1;
+    d->dv[v] = 0;
+    d->hmod[v] = 1;
+  }
+}
+
+void cb_pre_launch(b2o_exec *ex, int32_t loop) {
+  AppDev *d = D(ex);
+  const b2o_loop_info &li = d->app->info->loops[loop];
+  for (int i = 0; i < li.reads.n && !ex->stop; ++i) {
+    int v = li.reads.vars[i];
+    if (VI(d, v).is_array) ensure_dev(d, v, &d->acc.unplanned_bytes);
+    else ensure_host(d, v);
+  }
+  for (int i = 0; i < li.writes.n && !ex->stop; ++i) {
+    int v = li.writes.vars[i];
+    if (VI(d, v).is_array && d->mode == B2O_MODE_COHERENT) prepare_dev_write(d, v, &d->acc.unplanned_bytes);
+  }
+}
+
+void cb_launch(b2o_exec *ex, int32_t loop, void *args, uint32_t args_bytes, uint32_t total) {
+  AppDev *d = D(ex);
+  if (args == nullptr || total == 0) {
+    set_error(d, B2O_RUNTIME_ERROR, "loop " + std::to_string(loop) + ": iteration space exceeds 2^32");
+    return;
+  }
+  (void)args_bytes;
+  const uint32_t threads = 256;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>(((uint64_t)total + threads - 1) / threads, 0x7fffffffu);
+  void *params[] = {args};
+  if (!cu_ok(d, drv.launchKernel(d->kfun[loop], blocks, 1, 1, threads, 1, 1, 0, (CUstream)d->w->stream, params,
+                               nullptr),
+             "cuLaunchKernel"))
+    return;
+  d->acc.launches++;
+  const b2o_loop_info &li = d->app->info->loops[loop];
+  for (int i = 0; i < li.writes.n; ++i) {
+    int v = li.writes.vars[i];
+    d->dv[v] = 1;
+    d->hv[v] = 0;
+    if (VI(d, v).is_array) d->dev_dirty[v] = 1;
+  }
+}
+
+void cb_hook(b2o_exec *ex, int32_t loop, int32_t side) {
+  AppDev *d = D(ex);
+  for (const b2o_directive &dir : d->hooks[side][loop]) {
+    if (ex->stop) return;
+    int v = dir.var_id;
+    d->acc.directive_execs++;
+    size_t bytes = var_bytes(d, v);
+    bool array = VI(d, v).is_array;
+    if (dir.dir == B2O_DIR_H2D) {
+      if (!array) continue;  // scalar value rides in the next launch's arguments
+      if (d->mode == B2O_MODE_COHERENT && d->dv[v]) {
+        d->acc.elided_bytes += bytes;
+      } else {
+        copy_h2d(d, v);
+        d->acc.planned_bytes += bytes;
+      }
+      d->dv[v] = 1;
+    } else {
+      if (d->mode == B2O_MODE_COHERENT && d->hv[v]) {
+        d->acc.elided_bytes += bytes;
+      } else {
+        copy_d2h(d, v);
+        d->acc.planned_bytes += bytes;
+      }
+      d->hv[v] = 1;
+    }
+  }
+}
+
+void cb_block(b2o_exec *ex, int32_t block) {
+  AppDev *d = D(ex);
+  const b2o_op_info &op = d->app->info->blocks[block];
+  // a library call owns its operand transfers (as cuBLAS/cuFFT on host data)
+  int saved = d->mode;
+  d->mode = B2O_MODE_COHERENT;
+  ensure_dev(d, op.in0, &d->acc.block_bytes);
+  if (op.in1 >= 0) ensure_dev(d, op.in1, &d->acc.block_bytes);
+  d->dv[op.out] = 1;  // fully overwritten
+  d->mode = saved;
+  if (ex->stop) return;
+  int rc = 0;
+  if (op.op == B2O_OP_GEMM) {
+    if (d->app->info->precision != B2O_F32) {
+      set_error(d, B2O_RUNTIME_ERROR, "cublas_gemm replacement supports fp32 apps only");
+      return;
+    }
+    rc = b2o_gemm_f32((const float *)d->dev[op.in0], (const float *)d->dev[op.in1], (float *)d->dev[op.out],
+                      op.m, op.n, op.k, d->w->stream);
+  } else {
+    if (d->app->info->precision != B2O_F32) {
+      set_error(d, B2O_RUNTIME_ERROR, "cufft_exec replacement supports fp32 apps only");
+      return;
+    }
+    rc = b2o_fft2d_c64((const float *)d->dev[op.in0], (float *)d->dev[op.out], op.n, d->w->stream);
+  }
+  if (rc != 0) {
+    set_error(d, B2O_RUNTIME_ERROR, std::string("block kernel failed: ") + g_err);
+    return;
+  }
+  cuda_ok(d, cudaGetLastError(), "block launch");
+  d->acc.launches++;
+  d->dv[op.out] = 1;
+  d->hv[op.out] = 0;
+  d->dev_dirty[op.out] = 1;
+}
+
+void cb_external(b2o_exec *ex, int32_t call) {
+  AppDev *d = D(ex);
+  const b2o_op_info &op = d->app->info->calls[call];
+  if (op.op < 0) {
+    set_error(d, B2O_RUNTIME_ERROR, "opaque call without a CPU binding");
+    return;
+  }
+  ensure_host(d, op.in0);
+  if (op.in1 >= 0) ensure_host(d, op.in1);
+  ensure_host(d, op.out);
+  if (ex->stop) return;
+  int elem = VI(d, op.out).elem;
+  if (op.op == B2O_OP_GEMM) {
+    b2o_cpu_gemm(d->host[op.in0], d->host[op.in1], d->host[op.out], op.m, op.n, op.k, elem);
+  } else {
+    b2o_cpu_fft2d(d->host[op.in0], d->host[op.out], op.n, elem);
+  }
+  d->hv[op.out] = 1;
+  d->dv[op.out] = 0;
+  d->hmod[op.out] = 1;
+}
+
+// ---------------------------------------------------------------------------
+// app state
+// ---------------------------------------------------------------------------
+
+int load_host_module(AppShared *a) {
+  a->dl = dlopen(a->host_path.c_str(), RTLD_NOW | RTLD_LOCAL);
+  if (!a->dl) return fail("dlopen %s: %s", a->host_path.c_str(), dlerror());
+  auto info = (b2o_mod_info_fn)dlsym(a->dl, "b2o_mod_info");
+  a->run = (b2o_mod_run_fn)dlsym(a->dl, "b2o_mod_run");
+  if (!info || !a->run) return fail("module %s lacks b2o_mod_info/b2o_mod_run", a->host_path.c_str());
+  a->info = info();
+  if (a->info->abi != B2O_MODULE_ABI) return fail("module ABI %d != runtime ABI %d", a->info->abi, B2O_MODULE_ABI);
+  std::ifstream f(a->cubin_path, std::ios::binary);
+  if (!f) return fail("cannot read cubin %s", a->cubin_path.c_str());
+  a->image.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  a->image.push_back(0);
+  a->initial.resize(a->info->n_vars);
+  for (int v = 0; v < a->info->n_vars; ++v) {
+    const b2o_var_info &vi = a->info->vars[v];
+    a->initial[v].assign(vi.is_array ? (size_t)vi.length * elem_bytes(vi.elem) : elem_bytes(vi.elem), 0);
+  }
+  return 0;
+}
+
+int make_replica(AppShared *a, Worker *w, AppDev **out) {
+  auto d = std::make_unique<AppDev>();
+  d->app = a;
+  d->w = w;
+  const b2o_module_info *info = a->info;
+  int nv = info->n_vars, nl = info->n_loops;
+  if (cudaSetDevice(w->device) != cudaSuccess) return fail("cudaSetDevice(%d)", w->device);
+  cudaFree(0);
+  CUresult r = drv.moduleLoadData(&d->mod, a->image.data());
+  if (r != CUDA_SUCCESS) {
+    const char *s = nullptr;
+    drv.getErrorString(r, &s);
+    return fail("cuModuleLoadData: %s", s ? s : "?");
+  }
+  d->kfun.assign(nl, nullptr);
+  for (int l = 0; l < nl; ++l) {
+    if (!info->loops[l].kernel) continue;
+    r = drv.moduleGetFunction(&d->kfun[l], d->mod, info->loops[l].kernel);
+    if (r != CUDA_SUCCESS) return fail("kernel %s missing from cubin", info->loops[l].kernel);
+  }
+  d->host.assign(nv, nullptr);
+  d->dev.assign(nv, nullptr);
+  d->dev_pristine.assign(nv, nullptr);
+  if (cudaHostAlloc(&d->cells, 8 * (size_t)std::max(nv, 1), cudaHostAllocPortable) != cudaSuccess)
+    return fail("pinned alloc of scalar cells");
+  if (cudaHostAlloc(&d->slab_init, 8 * (size_t)std::max(nv, 1), cudaHostAllocPortable) != cudaSuccess)
+    return fail("pinned alloc of slab image");
+  memset(d->cells, 0, 8 * (size_t)std::max(nv, 1));
+  memset(d->slab_init, 0, 8 * (size_t)std::max(nv, 1));
+  if (cudaMalloc(&d->slab, 8 * (size_t)std::max(nv, 1)) != cudaSuccess) return fail("device slab alloc");
+  for (int v = 0; v < nv; ++v) {
+    const b2o_var_info &vi = info->vars[v];
+    size_t bytes = a->initial[v].size();
+    if (!vi.is_array) {
+      d->host[v] = (char *)d->cells + 8 * v;
+      memcpy((char *)d->slab_init + 8 * v, a->initial[v].data(), bytes);
+      continue;
+    }
+    if (cudaHostAlloc(&d->host[v], bytes, cudaHostAllocPortable) != cudaSuccess)
+      return fail("pinned alloc %zu B for %s", bytes, vi.name);
+    if (cudaMalloc(&d->dev[v], bytes) != cudaSuccess) return fail("device alloc %zu B for %s", bytes, vi.name);
+    if (cudaMemcpy(d->dev[v], a->initial[v].data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail("initial upload of %s", vi.name);
+    if (vi.written) {
+      if (cudaMalloc(&d->dev_pristine[v], bytes) != cudaSuccess) return fail("pristine alloc for %s", vi.name);
+      if (cudaMemcpy(d->dev_pristine[v], d->dev[v], bytes, cudaMemcpyDeviceToDevice) != cudaSuccess)
+        return fail("pristine copy of %s", vi.name);
+    }
+    memcpy(d->host[v], a->initial[v].data(), bytes);
+  }
+  d->hv.assign(nv, 1);
+  d->dv.assign(nv, 0);
+  d->hmod.assign(nv, 0);
+  d->dev_dirty.assign(nv, 0);
+  d->is_root.assign(std::max(nl, 1), 0);
+  d->dev_inside.assign(std::max(nl, 1), 0);
+  d->hook_mask.assign(std::max(nl, 1), 0);
+  d->hooks[0].assign(nl, {});
+  d->hooks[1].assign(nl, {});
+  b2o_exec &ex = d->ex;
+  ex.rt = d.get();
+  ex.host = d->host.data();
+  ex.dev = d->dev.data();
+  ex.slab = d->slab;
+  ex.is_root = d->is_root.data();
+  ex.dev_inside = d->dev_inside.data();
+  ex.hook_mask = d->hook_mask.data();
+  ex.hook = cb_hook;
+  ex.host_access = cb_host_access;
+  ex.pre_launch = cb_pre_launch;
+  ex.launch = cb_launch;
+  ex.block = cb_block;
+  ex.external = cb_external;
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail("replica setup sync");
+  *out = d.get();
+  a->per_worker[w->index] = std::move(d);
+  return 0;
+}
+
+// restore pristine state; host copies valid, device copies "not present"
+void reset_state(AppDev *d) {
+  const b2o_module_info *info = d->app->info;
+  for (int v = 0; v < info->n_vars; ++v) {
+    const b2o_var_info &vi = info->vars[v];
+    if (!vi.is_array) {
+      memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
+    } else if (vi.written) {
+      memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
+      if (d->dev_dirty[v])
+        cudaMemcpyAsync(d->dev[v], d->dev_pristine[v], d->app->initial[v].size(), cudaMemcpyDeviceToDevice,
+                        d->w->stream);
+    }
+    d->dev_dirty[v] = 0;
+  }
+  cudaMemcpyAsync(d->slab, d->slab_init, 8 * (size_t)std::max(info->n_vars, 1), cudaMemcpyHostToDevice,
+                  d->w->stream);
+  cudaStreamSynchronize(d->w->stream);
+  std::fill(d->hv.begin(), d->hv.end(), 1);
+  std::fill(d->dv.begin(), d->dv.end(), 0);
+  std::fill(d->hmod.begin(), d->hmod.end(), 0);
+  d->acc = b2o_result{};
+  d->err_validity = B2O_VALID;
+  d->err.clear();
+  d->ex.stop = 0;
+}
+
+std::string configure_pattern(AppDev *d, const Job &j) {
+  const b2o_module_info *info = d->app->info;
+  int nl = info->n_loops;
+  if (j.pat.n_loops != nl) return "pattern covers " + std::to_string(j.pat.n_loops) + " loops, program has " +
+                                 std::to_string(nl);
+  std::fill(d->is_root.begin(), d->is_root.end(), 0);
+  std::fill(d->dev_inside.begin(), d->dev_inside.end(), 0);
+  std::fill(d->hook_mask.begin(), d->hook_mask.end(), 0);
+  for (int l = 0; l < nl; ++l) {
+    d->hooks[0][l].clear();
+    d->hooks[1][l].clear();
+  }
+  for (int l = 0; l < nl; ++l) {
+    if (info->loops[l].device_op) {
+      for (int p = l; p >= 0; p = info->loops[p].parent) d->dev_inside[p] = 1;
+    }
+    if (!j.roots[l]) continue;
+    if (!info->loops[l].kernel)
+      return "loop " + std::to_string(l) + " cannot run on the GPU: " +
+             (info->loops[l].why_not ? info->loops[l].why_not : "?");
+    d->is_root[l] = 1;
+    for (int p = info->loops[l].parent; p >= 0; p = info->loops[p].parent) d->dev_inside[p] = 1;
+  }
+  for (const b2o_directive &dir : j.dirs) {
+    if (dir.anchor_loop < 0 || dir.anchor_loop >= nl || dir.var_id < 0 || dir.var_id >= info->n_vars ||
+        (dir.side != 0 && dir.side != 1))
+      return "malformed transfer directive";
+    d->hooks[dir.side][dir.anchor_loop].push_back(dir);
+    d->hook_mask[dir.anchor_loop] |= (uint8_t)(1 << dir.side);
+  }
+  return "";
+}
+
+void compare_outputs(AppDev *d, b2o_result &r) {
+  AppShared *a = d->app;
+  const b2o_module_info *info = a->info;
+  double worst = 0.0;
+  uint64_t bad = 0;
+  std::string first_bad;
+  for (int o = 0; o < info->n_outputs; ++o) {
+    const b2o_output_info &oi = info->outputs[o];
+    auto it = a->reference.find(oi.var);
+    if (it == a->reference.end()) continue;
+    const b2o_var_info &vi = info->vars[oi.var];
+    int64_t n = vi.is_array ? vi.length : 1;
+    const char *cand = (const char *)d->host[oi.var];
+    const char *ref = it->second.data();
+    auto val = [&](const char *base, int64_t i) -> double {
+      if (vi.elem == B2O_I32) return (double)((const int32_t *)base)[i];
+      if (vi.elem == B2O_F32) return (double)((const float *)base)[i];
+      return ((const double *)base)[i];
+    };
+    uint64_t nbad = 0;
+    double w = 0.0;
+    if (oi.mode == B2O_CMP_NORMWISE) {
+      double num = 0.0, den = 0.0;
+      for (int64_t i = 0; i < n; ++i) {
+        double c = val(cand, i), rr = val(ref, i);
+        num += (c - rr) * (c - rr);
+        den += rr * rr;
+      }
+      double rel = std::sqrt(num) / std::max(std::sqrt(den), 1e-300);
+      if (!(rel <= oi.rel_tol)) nbad = 1;
+      w = rel;
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        double c = val(cand, i), rr = val(ref, i);
+        double diff = std::fabs(c - rr);
+        if (!(diff <= std::max(oi.rel_tol * std::fabs(rr), 1e-12))) ++nbad;
+        double rel = diff / std::max(std::fabs(rr), 1e-30);
+        if (rel > w || std::isnan(rel)) w = std::isnan(rel) ? INFINITY : rel;
+      }
+    }
+    worst = std::max(worst, w);
+    if (nbad && first_bad.empty()) first_bad = vi.name;
+    bad += nbad;
+  }
+  r.max_rel_err = worst;
+  r.mismatches = bad;
+  if (bad && r.validity == B2O_VALID) {
+    r.validity = B2O_NUMERIC_MISMATCH;
+    snprintf(r.diag, sizeof r.diag, "output %s differs from the reference (%llu elements, max rel %.3g)",
+             first_bad.c_str(), (unsigned long long)bad, worst);
+  }
+}
+
+void execute(Worker *w, Job &j) {
+  b2o_result &r = j.res;
+  r = b2o_result{};
+  r.worker = w->index;
+  if (w->broken) {
+    r.validity = B2O_RUNTIME_ERROR;
+    snprintf(r.diag, sizeof r.diag, "device lost: %s", w->broken_why.c_str());
+    return;
+  }
+  AppDev *d = j.app->per_worker[w->index].get();
+  if (!d) {
+    r.validity = B2O_RUNTIME_ERROR;
+    snprintf(r.diag, sizeof r.diag, "app not finalized on worker %d", w->index);
+    return;
+  }
+  cudaSetDevice(w->device);
+  std::string why = configure_pattern(d, j);
+  if (!why.empty()) {
+    r.validity = B2O_COMPILE_ERROR;
+    snprintf(r.diag, sizeof r.diag, "%s", why.c_str());
+    return;
+  }
+  d->mode = j.pat.mode == B2O_MODE_LITERAL ? B2O_MODE_LITERAL : B2O_MODE_COHERENT;
+  int reps = std::max(1, j.pat.repeats);
+  double best = INFINITY;
+  b2o_result keep{};
+  for (int rep = 0; rep < reps; ++rep) {
+    reset_state(d);
+    w->timed_out = 0;
+    w->deadline_ns = j.pat.timeout_s > 0 ? now_ns() + (int64_t)(j.pat.timeout_s * 1e9) : 0;
+    w->running = &d->ex;
+    auto t0 = Clock::now();
+    j.app->run(&d->ex);
+    cudaError_t e = cudaStreamSynchronize(w->stream);
+    auto t1 = Clock::now();
+    w->running = nullptr;
+    w->deadline_ns = 0;
+    if (e != cudaSuccess) cuda_ok(d, e, "stream sync");
+    if (w->timed_out) set_error(d, B2O_TIMEOUT, "pattern exceeded its timeout");
+    if (d->err_validity != B2O_VALID) break;
+    double t = std::chrono::duration<double>(t1 - t0).count();
+    if (t < best) {
+      best = t;
+      keep = d->acc;
+    }
+  }
+  if (d->err_validity != B2O_VALID) {
+    r = d->acc;
+    r.worker = w->index;
+    r.validity = d->err_validity;
+    snprintf(r.diag, sizeof r.diag, "%s", d->err.c_str());
+    cudaStreamSynchronize(w->stream);
+    return;
+  }
+  r = keep;
+  r.worker = w->index;
+  r.time_s = best;
+  r.validity = B2O_VALID;
+  // outputs must be readable on the host for the comparison (untimed)
+  const b2o_module_info *info = j.app->info;
+  for (int o = 0; o < info->n_outputs; ++o) {
+    int v = info->outputs[o].var;
+    if (!d->hv[v] && d->mode == B2O_MODE_COHERENT) {
+      copy_d2h(d, v);
+      d->hv[v] = 1;
+      r.epilogue_bytes += var_bytes(d, v);
+    }
+  }
+  if (d->err_validity != B2O_VALID) {
+    r.validity = d->err_validity;
+    snprintf(r.diag, sizeof r.diag, "%s", d->err.c_str());
+    return;
+  }
+  compare_outputs(d, r);
+  d->have_final = true;
+}
+
+void worker_loop(Worker *w) {
+  cudaSetDevice(w->device);
+  for (;;) {
+    Job *j = nullptr;
+    {
+      std::unique_lock<std::mutex> lk(g_rt->qmu);
+      g_rt->qcv.wait(lk, [&] {
+        if (g_rt->stopping) return true;
+        for (Job *q : g_rt->queue)
+          if (q->pat.device < 0 || q->pat.device == w->index) return true;
+        return false;
+      });
+      if (g_rt->stopping) return;
+      for (auto it = g_rt->queue.begin(); it != g_rt->queue.end(); ++it) {
+        if ((*it)->pat.device < 0 || (*it)->pat.device == w->index) {
+          j = *it;
+          g_rt->queue.erase(it);
+          break;
+        }
+      }
+    }
+    if (!j) continue;
+    execute(w, *j);
+    Batch *b = j->batch;
+    std::lock_guard<std::mutex> lk(b->mu);
+    if (--b->remaining == 0) b->cv.notify_all();
+  }
+}
+
+void watchdog_loop() {
+  while (true) {
+    {
+      std::lock_guard<std::mutex> lk(g_rt->qmu);
+      if (g_rt->stopping) return;
+    }
+    int64_t t = now_ns();
+    for (auto &w : g_rt->workers) {
+      int64_t dl = w->deadline_ns.load();
+      b2o_exec *ex = w->running.load();
+      if (dl > 0 && ex && t > dl) {
+        w->timed_out = 1;
+        ex->stop = 1;
+      }
+    }
+    std::this_thread::sleep_for(std::chrono::milliseconds(2));
+  }
+}
+
+AppShared *find_app(uint64_t id) {
+  if (!g_rt) return nullptr;
+  auto it = g_rt->apps.find(id);
+  return it == g_rt->apps.end() ? nullptr : it->second.get();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char *b2o_last_error(void) { return g_err.c_str(); }
+int b2o_abi_version(void) { return B2O_ABI_VERSION; }
+
+int b2o_init(const int32_t *device_ids, int32_t n) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_rt) return fail("b2o already initialised");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return fail("no CUDA device visible");
+  cudaFree(0);
+  if (!load_driver_api()) return fail("CUDA driver entry points unavailable");
+  g_rt = new Runtime();
+  std::vector<int> ids;
+  if (n <= 0 || !device_ids) {
+    for (int i = 0; i < count; ++i) ids.push_back(i);
+  } else {
+    ids.assign(device_ids, device_ids + n);
+  }
+  for (size_t i = 0; i < ids.size(); ++i) {
+    if (ids[i] < 0 || ids[i] >= count) {
+      delete g_rt;
+      g_rt = nullptr;
+      return fail("device %d out of range (%d visible)", ids[i], count);
+    }
+    auto w = std::make_unique<Worker>();
+    w->index = (int)i;
+    w->device = ids[i];
+    cudaSetDevice(w->device);
+    if (cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete g_rt;
+      g_rt = nullptr;
+      return fail("stream creation on device %d", ids[i]);
+    }
+    g_rt->workers.push_back(std::move(w));
+  }
+  for (auto &w : g_rt->workers) w->th = std::thread(worker_loop, w.get());
+  g_rt->watchdog = std::thread(watchdog_loop);
+  return 0;
+}
+
+int b2o_num_workers(void) { return g_rt ? (int)g_rt->workers.size() : 0; }
+
+int b2o_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_rt) return 0;
+  {
+    std::lock_guard<std::mutex> q(g_rt->qmu);
+    g_rt->stopping = true;
+  }
+  g_rt->qcv.notify_all();
+  for (auto &w : g_rt->workers) w->th.join();
+  g_rt->watchdog.join();
+  for (auto &kv : g_rt->apps) {
+    AppShared *a = kv.second.get();
+    for (auto &d : a->per_worker) {
+      if (!d) continue;
+      cudaSetDevice(d->w->device);
+      for (void *p : d->dev) if (p) cudaFree(p);
+      for (void *p : d->dev_pristine) if (p) cudaFree(p);
+      for (size_t v = 0; v < d->host.size(); ++v)
+        if (a->info->vars[v].is_array && d->host[v]) cudaFreeHost(d->host[v]);
+      if (d->cells) cudaFreeHost(d->cells);
+      if (d->slab_init) cudaFreeHost(d->slab_init);
+      if (d->slab) cudaFree(d->slab);
+      if (d->mod) drv.moduleUnload(d->mod);
+    }
+  }
+  for (auto &w : g_rt->workers) {
+    cudaSetDevice(w->device);
+    cudaStreamDestroy(w->stream);
+  }
+  delete g_rt;
+  g_rt = nullptr;
+  return 0;
+}
+
+int b2o_app_create(const char *host_module, const char *cubin, uint64_t *app) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_rt) return fail("b2o_init not called");
+  auto a = std::make_unique<AppShared>();
+  a->host_path = host_module;
+  a->cubin_path = cubin;
+  if (load_host_module(a.get()) != 0) return -1;
+  a->per_worker.resize(g_rt->workers.size());
+  uint64_t id = g_rt->next_id++;
+  g_rt->apps[id] = std::move(a);
+  *app = id;
+  return 0;
+}
+
+int b2o_app_set_initial(uint64_t app, int32_t var_id, const void *data, uint64_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a) return fail("unknown app %llu", (unsigned long long)app);
+  if (a->finalized) return fail("app already finalized");
+  if (var_id < 0 || var_id >= a->info->n_vars) return fail("bad var id %d", var_id);
+  if (bytes != a->initial[var_id].size())
+    return fail("var %s: %llu bytes given, %zu expected", a->info->vars[var_id].name, (unsigned long long)bytes,
+                a->initial[var_id].size());
+  memcpy(a->initial[var_id].data(), data, bytes);
+  return 0;
+}
+
+int b2o_app_set_reference(uint64_t app, int32_t var_id, const void *data, uint64_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a) return fail("unknown app");
+  if (var_id < 0 || var_id >= a->info->n_vars) return fail("bad var id %d", var_id);
+  if (bytes != a->initial[var_id].size()) return fail("reference size mismatch for %s", a->info->vars[var_id].name);
+  a->reference[var_id].assign((const char *)data, (const char *)data + bytes);
+  return 0;
+}
+
+int b2o_app_finalize(uint64_t app) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a) return fail("unknown app");
+  if (a->finalized) return 0;
+  for (auto &w : g_rt->workers) {
+    AppDev *d = nullptr;
+    if (make_replica(a, w.get(), &d) != 0) return -1;
+  }
+  a->finalized = true;
+  bool need_ref = false;
+  for (int o = 0; o < a->info->n_outputs; ++o)
+    if (!a->reference.count(a->info->outputs[o].var)) need_ref = true;
+  if (need_ref) {
+    // the original program: every loop on the CPU (genome 0...0)
+    Worker *w = g_rt->workers[0].get();
+    AppDev *d = a->per_worker[0].get();
+    Job j{};
+    j.app = a;
+    j.pat.n_loops = a->info->n_loops;
+    j.pat.repeats = 1;
+    j.pat.device = 0;
+    j.roots.assign(a->info->n_loops, 0);
+    // run on the caller thread with the worker's stream: the worker is idle
+    // because no batch can reference this app before finalize returns
+    execute(w, j);
+    if (j.res.validity != B2O_VALID && j.res.validity != B2O_NUMERIC_MISMATCH)
+      return fail("reference run failed: %s", j.res.diag);
+    a->ref_time = j.res.time_s;
+    for (int o = 0; o < a->info->n_outputs; ++o) {
+      int v = a->info->outputs[o].var;
+      if (a->reference.count(v)) continue;
+      a->reference[v].assign((const char *)d->host[v], (const char *)d->host[v] + a->initial[v].size());
+    }
+  }
+  return 0;
+}
+
+double b2o_app_reference_time(uint64_t app) {
+  AppShared *a = find_app(app);
+  return a ? a->ref_time : -1.0;
+}
+
+int b2o_app_get_reference(uint64_t app, int32_t var_id, void *out, uint64_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a) return fail("unknown app");
+  auto it = a->reference.find(var_id);
+  if (it == a->reference.end()) return fail("no reference for var %d", var_id);
+  if (bytes != it->second.size()) return fail("reference size mismatch");
+  memcpy(out, it->second.data(), bytes);
+  return 0;
+}
+
+int b2o_app_read(uint64_t app, int32_t worker, int32_t var_id, void *out, uint64_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a || worker < 0 || worker >= (int)a->per_worker.size() || !a->per_worker[worker])
+    return fail("unknown app/worker");
+  AppDev *d = a->per_worker[worker].get();
+  if (var_id < 0 || var_id >= a->info->n_vars) return fail("bad var id");
+  if (bytes != a->initial[var_id].size()) return fail("size mismatch");
+  memcpy(out, d->host[var_id], bytes);
+  return 0;
+}
+
+int b2o_app_destroy(uint64_t app) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a) return fail("unknown app");
+  for (auto &d : a->per_worker) {
+    if (!d) continue;
+    cudaSetDevice(d->w->device);
+    cudaStreamSynchronize(d->w->stream);
+    for (void *p : d->dev) if (p) cudaFree(p);
+    for (void *p : d->dev_pristine) if (p) cudaFree(p);
+    for (size_t v = 0; v < d->host.size(); ++v)
+      if (a->info->vars[v].is_array && d->host[v]) cudaFreeHost(d->host[v]);
+    if (d->cells) cudaFreeHost(d->cells);
+    if (d->slab_init) cudaFreeHost(d->slab_init);
+    if (d->slab) cudaFree(d->slab);
+    if (d->mod) drv.moduleUnload(d->mod);
+  }
+  if (a->dl) dlclose(a->dl);
+  g_rt->apps.erase(app);
+  return 0;
+}
+
+int b2o_submit(uint64_t app, const b2o_pattern *patterns, int32_t n, uint64_t *batch) {
+  std::unique_lock<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a) return fail("unknown app");
+  if (!a->finalized) return fail("app not finalized");
+  auto b = std::make_unique<Batch>();
+  b->jobs.resize(n);
+  b->remaining = n;
+  for (int i = 0; i < n; ++i) {
+    Job &j = b->jobs[i];
+    j.app = a;
+    j.pat = patterns[i];
+    j.roots.assign(patterns[i].gpu_root, patterns[i].gpu_root + std::max(patterns[i].n_loops, 0));
+    j.dirs.assign(patterns[i].directives, patterns[i].directives + std::max(patterns[i].n_directives, 0));
+    j.batch = b.get();
+    j.slot = i;
+    if (j.pat.device >= (int)g_rt->workers.size()) return fail("pattern %d targets worker %d", i, j.pat.device);
+  }
+  uint64_t id = g_rt->next_id++;
+  Batch *raw = b.get();
+  g_rt->batches[id] = std::move(b);
+  lk.unlock();
+  {
+    std::lock_guard<std::mutex> q(g_rt->qmu);
+    std::vector<Job *> order;
+    for (auto &j : raw->jobs) order.push_back(&j);
+    std::stable_sort(order.begin(), order.end(),
+                     [](const Job *x, const Job *y) { return x->pat.priority > y->pat.priority; });
+    for (Job *j : order) g_rt->queue.push_back(j);
+  }
+  g_rt->qcv.notify_all();
+  *batch = id;
+  return 0;
+}
+
+int b2o_wait(uint64_t batch, b2o_result *results, int32_t n, double timeout_s) {
+  Batch *b = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_rt) return fail("not initialised");
+    auto it = g_rt->batches.find(batch);
+    if (it == g_rt->batches.end()) return fail("unknown batch");
+    b = it->second.get();
+  }
+  {
+    std::unique_lock<std::mutex> lk(b->mu);
+    if (timeout_s > 0) {
+      if (!b->cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return b->remaining == 0; }))
+        return fail("batch wait timed out");
+    } else {
+      b->cv.wait(lk, [&] { return b->remaining == 0; });
+    }
+  }
+  if (n != (int)b->jobs.size()) return fail("batch has %zu results, %d requested", b->jobs.size(), n);
+  for (int i = 0; i < n; ++i) results[i] = b->jobs[i].res;
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_rt->batches.erase(batch);
+  return 0;
+}
+
+}  // extern "C"
