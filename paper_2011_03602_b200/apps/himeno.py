@@ -55,7 +55,10 @@ def _s0(J: int, K: int) -> str:
     )
 
 
-def source(size: str | tuple[int, int, int] = "M", nn: int = 4, form: str = "inline") -> str:
+def source(size: str | tuple[int, int, int] = "M", nn: int = 4, form: str = "inline", read_p: bool = True) -> str:
+    """``read_p=False`` drops the final host read of ``p``: the reference plan
+    then never fetches ``p``, the hole the coherent variable
+    manager repairs."""
     I, J, K = SIZES[size] if isinstance(size, str) else size
     n = I * J * K
     x = _idx(J, K)
@@ -89,6 +92,8 @@ def source(size: str | tuple[int, int, int] = "M", nn: int = 4, form: str = "inl
         raise ValueError(f"unknown Himeno form {form!r}")
     out += loops([f"p[{x}] = wrk2[{x}];"])
     tail = "gosa + p[0] + gs[0]" if form == "inline" else "gosa + p[0]"
+    if not read_p:
+        tail = tail.replace(" + p[0]", "")
     out += f"  }}\n  chk = {tail};\n}}\n"
     return out
 

@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-4"
+COMPILER_VERSION = "b2o-compiler-6"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 
@@ -274,8 +274,11 @@ class _Gen:
     def T(self, vid: int) -> str:
         return ctype(self.prog, vid, self.precision)
 
-    def access_set(self, reads, writes) -> int:
-        key = (tuple(sorted(set(reads) | set(writes))), tuple(sorted(writes)))
+    def access_set(self, need, writes) -> int:
+        """Host footprint of a statement / fast loop / loop header: ``need``
+        must be valid on the host before it runs, ``writes`` are host-dirty
+        after it."""
+        key = (tuple(sorted(need)), tuple(sorted(writes)))
         if key not in self.set_ids:
             self.set_ids[key] = len(self.sets)
             self.sets.append(key)
@@ -288,6 +291,16 @@ class _Gen:
 
     def subtree_access(self, lid):
         return self.prog.subtree_access(lid, self.extra_writes)
+
+    def fast_footprint(self, lid):
+        """(need, writes) of running loop ``lid`` on the CPU: every array it
+        touches, scalars only when their first access may be a read."""
+        reads, writes = self.subtree_access(lid)
+        need = set()
+        for v in reads | writes:
+            if self.prog.vars[v].is_array or _first_access_is_read(self.prog, lid, v):
+                need.add(v)
+        return need, writes
 
     @staticmethod
     def host_name(vid: int, is_array: bool) -> str:
@@ -372,7 +385,8 @@ class _Gen:
                 reads, writes = prog.stmt_access(st)
                 if st.kind == "decl" and st.init is None:
                     continue
-                sid = self.access_set(reads, writes)
+                need = reads | {v for v in writes if prog.vars[v].is_array}
+                sid = self.access_set(need, writes)
                 out.append(pad + f"ex->host_access(ex, {sid}); if (ex->stop) return;")
                 if st.kind == "decl":
                     out.append(pad + f"S{st.var} = {render(st.init, self.host_name)};")
@@ -397,12 +411,12 @@ class _Gen:
         if self.nests[lid].kernel:
             branches.append((f"ex->is_root[{lid}]", [f"launch_L{lid}(ex); if (ex->stop) return;"]))
         if not self.device_op[lid]:
-            sid = self.access_set(*self.subtree_access(lid))
+            sid = self.access_set(*self.fast_footprint(lid))
             branches.append((f"!ex->dev_inside[{lid}]",
                              [f"ex->host_access(ex, {sid}); if (ex->stop) return;",
                               f"fast_L{lid}(ex); if (ex->stop) return;"]))
-        hr, hw = prog.loop_header_access(lid)
-        hsid = self.access_set(hr, hw)
+        hneed = set(expr_vars(loop.lower)) | (set(expr_vars(loop.upper)) - {loop.index_var})
+        hsid = self.access_set(hneed, {loop.index_var})
         iv = f"S{loop.index_var}"
         inner = [f"ex->host_access(ex, {hsid}); if (ex->stop) return;",
                  f"for ({iv} = {render(loop.lower, self.host_name)}; {iv} < {render(loop.upper, self.host_name)}; "
@@ -453,7 +467,7 @@ class _Gen:
                        f"total *= a.n[{d}]; }}")
         if n.chain:
             out.append("  if (total == 0) {")
-            sid = self.access_set(*self.subtree_access(lid))
+            sid = self.access_set(*self.fast_footprint(lid))
             out.append(f"    ex->host_access(ex, {sid}); if (ex->stop) return;")
             out.append(f"    fast_L{lid}(ex); return;")
             out.append("  }")
@@ -713,7 +727,7 @@ def compile_program(doc: dict, spec: dict, cache_dir: Path | None = None) -> Com
         (tmp / "app_dev.cu").write_text(dev)
         (tmp / "app_host.cpp").write_text(host)
         inc = ["-I", str(CSRC), "-I", str(tmp)]
-        fmad = "true" if spec.get("fmad", True) else "false"
+        fmad = "true" if spec.get("fmad", False) else "false"
         nvcc = os.environ.get("NVCC", "nvcc")
         jobs = [
             ["g++", "-O3", "-std=c++17", "-shared", "-fPIC", "-ffp-contract=off", "-fno-fast-math", *inc,

@@ -661,9 +661,10 @@ void execute(Worker *w, Job &j) {
     w->running = nullptr;
     w->deadline_ns = 0;
     if (e != cudaSuccess) cuda_ok(d, e, "stream sync");
-    if (w->timed_out) set_error(d, B2O_TIMEOUT, "pattern exceeded its timeout");
-    if (d->err_validity != B2O_VALID) break;
     double t = std::chrono::duration<double>(t1 - t0).count();
+    if (w->timed_out || (j.pat.timeout_s > 0 && t > j.pat.timeout_s))
+      set_error(d, B2O_TIMEOUT, "pattern exceeded its timeout");
+    if (d->err_validity != B2O_VALID) break;
     if (t < best) {
       best = t;
       keep = d->acc;

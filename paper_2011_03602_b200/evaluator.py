@@ -189,7 +189,10 @@ class B200Evaluator:
             q.setdefault("timeout_s", self.timeout_seconds)
             q.setdefault("priority", float(p.get("cost_model_time", 0.0) or 0.0))
             pats.append(q)
-        return app.run(pats)
+        try:
+            return app.run(pats)
+        except B2OError as exc:
+            return [{"validity": "runtime_error", "time_s": None, "diag": str(exc)[-250:]} for _ in payloads]
 
     def measure_batch(self, requests) -> list:
         groups: dict[str, list[int]] = {}

@@ -155,6 +155,9 @@ def main() -> None:
     for form in ("inline", "temps"):
         m = parse_mini_source(himeno.source("XS", nn=3, form=form))
         out[f"himeno_xs_{form}"] = app_record(f"himeno_xs_{form}", m, himeno.spec("XS", form=form))
+    m = parse_mini_source(himeno.source("XS", nn=2, read_p=False))
+    out["himeno_xs_noread"] = app_record("himeno_xs_noread", m, himeno.spec("XS"), extra_genomes=("100100",),
+                                         all_genomes_cap=1)
     m = parse_mini_source(himeno.source((17, 9, 33), nn=2))
     out["himeno_17x9x33"] = app_record("himeno_17x9x33", m, himeno.spec((17, 9, 33)))
     m = parse_mini_source(matmul.source(48))
