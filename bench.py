@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark of the fitness-evaluation hot path on B200 (BASELINE.json config 2).
+
+Workload: Himeno size M (129x129x257), inline form, nn = 20 sweeps, executed
+under the all-GPU offload pattern (genome 100100: Jacobi i-nest and copy
+i-nest on the GPU, gosa reduction on the host) with the reference's hoisted
+transfer plan (tests/golden/himeno_M.json, produced by the reference).
+
+* ``value`` (GB/s): one step = the pattern's whole GPU launch sequence for one
+  app run (20 Jacobi + 20 copy launches), replayed on data already resident in
+  HBM, timed with CUDA events on the worker stream; algorithmic bytes =
+  (60 + 8) B per interior point per sweep.  The 239 MB working
+  set exceeds the 126 MB L2.
+* ``e2e``: the same metric through the public plugin call
+  (``B200Evaluator.measure_payloads``: host buffers, the plan's H2D/D2H, the
+  host gosa nest, output comparison), wall clock per call.
+* ``--impl reference``: the reference CPU implementation of the path (the C
+  restatement in oracle/, all-CPU genome, OpenMP on every host core).
+
+Under torchrun each rank drives its own GPU with its own replica (weak
+scaling, no data-path collective); the step time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+for p in (ROOT / "baseline" / "_ref",):
+    if p.exists():
+        sys.path.append(str(p))
+
+METRIC = "offloaded-app speedup vs CPU ref; Himeno GB/s; GA patterns evaluated/sec"
+WORKLOAD = "himeno_M"
+GENOME = "100100"
+SIZE = (129, 129, 257)
+BYTES_PER_POINT = 60 + 8  # Jacobi nest + copy nest (apps/himeno.py)
+
+
+def golden(name: str) -> dict:
+    return json.loads((ROOT / "tests" / "golden" / f"{name}.json").read_text())
+
+
+def interior(size) -> int:
+    return (size[0] - 2) * (size[1] - 2) * (size[2] - 2)
+
+
+def sweeps_of(doc: dict) -> int:
+    for v in doc["variables"]:
+        if v["name"] == "nn":
+            nn_id = v["id"]
+    for r in doc["regions"]:
+        for s in r["statements"]:
+            if s.get("decl") == nn_id and "init" in s:
+                return int(s["init"]["num"])
+    raise ValueError("nn not found")
+
+
+# ---------------------------------------------------------------------------
+# plumbing
+# ---------------------------------------------------------------------------
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo", rank=self.rank, world_size=self.world)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.out,
+                                         stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        self.out.flush()
+        rows = [ln.split(",") for ln in Path(self.out.name).read_text().splitlines() if ln.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for name, val in zip(names, r[5:9]):
+                    if val.strip().lower() in ("active", "1"):
+                        reasons.add(name)
+            except (ValueError, IndexError):
+                continue
+        busy = [s for s in sm if s > 0.5 * mx] if mx else sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks() -> dict:
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        return dict(json.loads(f.read_text()), source="measured")
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel: str) -> float | None:
+    """dram bytes (read + write) per launch from the committed ncu capture."""
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if not f.exists():
+        return None
+    data = json.loads(f.read_text())
+    k = data.get("kernels", {}).get(kernel)
+    return None if k is None else k.get("dram_bytes")
+
+
+# ---------------------------------------------------------------------------
+# arms
+# ---------------------------------------------------------------------------
+
+
+def cpu_run(doc: dict, spec: dict, openmp: bool, runs: int) -> tuple[float, int]:
+    from oracle.cgen import CProgram
+    from paper_2011_03602_b200 import appspec
+    from paper_2011_03602_b200.ir import Program
+
+    state = appspec.initial_state(Program(doc), spec)
+    prog = CProgram(doc, spec.get("precision", "fp32"), openmp=openmp, opt="-O3")
+    best = float("inf")
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        prog.run(state)
+        best = min(best, time.perf_counter() - t0)
+    cores = len(os.sched_getaffinity(0)) if openmp else 1
+    return best, cores
+
+
+def reference_arm(args, dist: Dist) -> None:
+    if dist.rank != 0:
+        return
+    g = golden(WORKLOAD)
+    nn = sweeps_of(g["doc"])
+    bytes_per_step = BYTES_PER_POINT * interior(SIZE) * nn
+    from oracle.cgen import CProgram
+    from paper_2011_03602_b200 import appspec
+    from paper_2011_03602_b200.ir import Program
+
+    state = appspec.initial_state(Program(g["doc"]), g["spec"])
+    prog = CProgram(g["doc"], "fp32", openmp=True, opt="-O3")
+    for _ in range(max(args.warmup, 0)):
+        prog.run(state)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        prog.run(state)
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    cores = len(os.sched_getaffinity(0))
+    value = bytes_per_step / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (Himeno initmt)",
+        "config": {"workload": f"{WORKLOAD} inline nn={nn}, all-CPU genome 000000", "size": list(SIZE),
+                   "sweeps": nn},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"one full Himeno M app run ({nn} sweeps) per step, C restatement (oracle/cgen.py) "
+                                   f"gcc -O3 OpenMP"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def b200_arm(args, dist: Dist) -> None:
+    from paper_2011_03602_b200.evaluator import B200Evaluator
+
+    g = golden(WORKLOAD)
+    nn = sweeps_of(g["doc"])
+    pts = interior(SIZE)
+    bytes_per_step = BYTES_PER_POINT * pts * nn
+    pat = g["patterns"][GENOME]
+    ev = B200Evaluator(g["spec"], devices=[dist.local_rank])
+    app = ev.app_for(g["doc"])  # compile (cached) + load + reference run (untimed)
+    # correctness of the benchmarked pattern first
+    check = ev.measure_payloads(g["doc"], [pat])[0]
+    if check["validity"] != "valid":
+        raise SystemExit(f"pattern {GENOME} invalid: {check}")
+    dist.barrier()
+    with Clocks(dist.local_rank) as clk:
+        rep = app.bench_replay(pat, warmup=max(args.warmup, 3), steps=args.steps)
+        dist.barrier()
+        e2e = []
+        for _ in range(max(1, args.warmup // 2)):
+            ev.measure_payloads(g["doc"], [pat])
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            r = ev.measure_payloads(g["doc"], [pat])[0]
+            e2e.append((time.perf_counter() - t0, r))
+        dist.barrier()
+    ms = dist.max(rep["ms_per_step"])
+    e2e_s = dist.max(statistics.median(t for t, _ in e2e))
+    last = e2e[-1][1]
+    value = dist.world * bytes_per_step / (ms * 1e-3) / 1e9
+    e2e_value = dist.world * bytes_per_step / e2e_s / 1e9
+    pk = peaks()
+    jac_loop = g["genome_loops"][0]  # the Jacobi i-loop is the first genome bit
+    kms = rep["kernel_ms"].get(jac_loop)
+    achieved = 60 * pts / (kms * 1e-3) / 1e9 if kms else None
+    if dist.rank != 0:
+        return
+    cpu_s, cores = cpu_run(g["doc"], g["spec"], openmp=True, runs=1)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (Himeno initmt)",
+        "config": {"workload": f"{WORKLOAD} inline nn={nn}, genome {GENOME} (Jacobi+copy nests on GPU, "
+                               "reference hoisted plan)", "size": list(SIZE), "sweeps": nn,
+                   "l2": "inputs larger than L2 (239 MB working set > 126 MB)", "parallelism": f"replicas{dist.world}"},
+        "gpu_launches": int(rep["launches_per_step"] * args.steps),
+        "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": int(last["h2d_bytes"]),
+                "d2h_bytes_per_step": int(last["d2h_bytes"]), "ms_per_call": round(e2e_s * 1e3, 3),
+                "app_run_ms": round(last["time_s"] * 1e3, 3), "call": "B200Evaluator.measure_payloads"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
+                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4) if achieved else None,
+                     "traffic": ncu_traffic(f"b2o_k{jac_loop}"), "kernel": f"b2o_k{jac_loop} (Himeno Jacobi nest)",
+                     "kernel_us": round(kms * 1e3, 2) if kms else None, "bytes_per_launch": 60 * pts,
+                     "peak_source": pk.get("source")},
+        "kernels_us": {f"b2o_k{k}": round(v * 1e3, 2) for k, v in rep["kernel_ms"].items()},
+        "cpu_baseline": {"value": round(bytes_per_step / cpu_s / 1e9, 3), "unit": "GB/s", "cores": cores,
+                         "kind": "port", "sample": f"one full Himeno M app run ({nn} sweeps), C restatement "
+                                                   "(oracle/cgen.py), gcc -O3 OpenMP, all-CPU genome"},
+        "app_speedup_vs_cpu": round(cpu_s / e2e_s, 2),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    args = ap.parse_args()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            reference_arm(args, dist)
+        else:
+            b200_arm(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -94,6 +94,8 @@ typedef struct {
   uint64_t directive_execs;  /* executed directive instances (== sum multiplicity) */
   uint64_t launches;         /* GPU kernels launched inside the timed region */
   uint64_t stale_reads;      /* LITERAL mode: accesses that saw stale data */
+  uint64_t h2d_bytes;        /* all host->device bytes inside the timed run */
+  uint64_t d2h_bytes;        /* all device->host bytes inside the timed run */
   char diag[256];
 } b2o_result;
 
@@ -115,6 +117,13 @@ int b2o_app_destroy(uint64_t app);
 
 int b2o_submit(uint64_t app, const b2o_pattern *patterns, int32_t n, uint64_t *batch);
 int b2o_wait(uint64_t batch, b2o_result *results, int32_t n, double timeout_s);
+
+/* device-resident replay (bench): run the pattern once recording every kernel
+ * launch, then re-issue that launch sequence `steps` times on the resident
+ * data, timed with CUDA events on the worker's stream.  kernel_ms[loop] is the
+ * mean device time of one launch of that loop's kernel (0 if never launched). */
+int b2o_bench_replay(uint64_t app, int32_t worker, const b2o_pattern *pattern, int32_t warmup, int32_t steps,
+                     double *ms_per_step, double *kernel_ms, int32_t n_loops, uint64_t *launches_per_step);
 
 /* hand-written sm_100a kernels behind the block replacements, on device
  * pointers, stream = cudaStream_t (NULL = default) */

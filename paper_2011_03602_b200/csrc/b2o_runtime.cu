@@ -94,6 +94,13 @@ struct AppDev {
   int err_validity = B2O_VALID;
   std::string err;
   bool have_final = false;
+  bool recording = false;
+  struct Launch {
+    int loop;
+    std::vector<char> args;
+    uint32_t total;
+  };
+  std::vector<Launch> log;
 };
 
 struct AppShared {
@@ -214,6 +221,7 @@ void copy_h2d(AppDev *d, int v) {
   cuda_ok(d, cudaMemcpyAsync(d->dev[v], d->host[v], var_bytes(d, v), cudaMemcpyHostToDevice, d->w->stream),
           "H2D copy");
   d->dev_dirty[v] = 1;
+  d->acc.h2d_bytes += var_bytes(d, v);
 }
 
 void copy_d2h(AppDev *d, int v) {
@@ -226,6 +234,7 @@ void copy_d2h(AppDev *d, int v) {
             "D2H scalar copy");
   }
   cuda_ok(d, cudaStreamSynchronize(d->w->stream), "D2H sync");
+  d->acc.d2h_bytes += var_bytes(d, v);
 }
 
 // make the host copy current (coherent mode)
@@ -305,6 +314,7 @@ void cb_launch(b2o_exec *ex, int32_t loop, void *args, uint32_t args_bytes, uint
   const uint32_t threads = 256;
   uint32_t blocks = (uint32_t)std::min<uint64_t>(((uint64_t)total + threads - 1) / threads, 0x7fffffffu);
   void *params[] = {args};
+  if (d->recording) d->log.push_back({loop, std::vector<char>((char *)args, (char *)args + args_bytes), total});
   if (!cu_ok(d, drv.launchKernel(d->kfun[loop], blocks, 1, 1, threads, 1, 1, 0, (CUstream)d->w->stream, params,
                                nullptr),
              "cuLaunchKernel"))
@@ -960,6 +970,89 @@ int b2o_app_destroy(uint64_t app) {
   }
   if (a->dl) dlclose(a->dl);
   g_rt->apps.erase(app);
+  return 0;
+}
+
+int b2o_bench_replay(uint64_t app, int32_t worker, const b2o_pattern *pattern, int32_t warmup, int32_t steps,
+                     double *ms_per_step, double *kernel_ms, int32_t n_loops, uint64_t *launches_per_step) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a || !a->finalized) return fail("unknown or unfinalized app");
+  if (worker < 0 || worker >= (int)a->per_worker.size()) return fail("bad worker");
+  AppDev *d = a->per_worker[worker].get();
+  Worker *w = d->w;
+  if (n_loops != a->info->n_loops) return fail("kernel_ms has %d slots, program has %d loops", n_loops,
+                                               a->info->n_loops);
+  cudaSetDevice(w->device);
+  Job j{};
+  j.app = a;
+  j.pat = *pattern;
+  j.roots.assign(pattern->gpu_root, pattern->gpu_root + pattern->n_loops);
+  j.dirs.assign(pattern->directives, pattern->directives + pattern->n_directives);
+  std::string why = configure_pattern(d, j);
+  if (!why.empty()) return fail("%s", why.c_str());
+  d->mode = B2O_MODE_COHERENT;
+  reset_state(d);
+  d->log.clear();
+  d->recording = true;
+  a->run(&d->ex);
+  d->recording = false;
+  if (cudaStreamSynchronize(w->stream) != cudaSuccess || d->err_validity != B2O_VALID)
+    return fail("recording run failed: %s", d->err.c_str());
+  if (d->log.empty()) return fail("pattern launches no kernel");
+  auto replay = [&]() -> bool {
+    for (auto &L : d->log) {
+      const uint32_t threads = 256;
+      uint32_t blocks = (uint32_t)(((uint64_t)L.total + threads - 1) / threads);
+      void *params[] = {L.args.data()};
+      if (drv.launchKernel(d->kfun[L.loop], blocks, 1, 1, threads, 1, 1, 0, (CUstream)w->stream, params,
+                           nullptr) != CUDA_SUCCESS)
+        return false;
+    }
+    return true;
+  };
+  for (int i = 0; i < warmup; ++i)
+    if (!replay()) return fail("replay launch failed");
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, w->stream);
+  for (int i = 0; i < steps; ++i)
+    if (!replay()) return fail("replay launch failed");
+  cudaEventRecord(e1, w->stream);
+  if (cudaEventSynchronize(e1) != cudaSuccess) return fail("replay failed: %s", cudaGetErrorString(cudaGetLastError()));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *ms_per_step = steps > 0 ? ms / steps : 0.0;
+  *launches_per_step = d->log.size();
+  // per-launch device time, one event pair per launch
+  std::vector<cudaEvent_t> ev(2 * d->log.size());
+  for (auto &e : ev) cudaEventCreate(&e);
+  std::vector<double> sum(n_loops, 0.0);
+  std::vector<int> cnt(n_loops, 0);
+  int passes = std::max(1, std::min(steps, 5));
+  for (int pss = 0; pss < passes; ++pss) {
+    for (size_t i = 0; i < d->log.size(); ++i) {
+      auto &L = d->log[i];
+      uint32_t blocks = (uint32_t)(((uint64_t)L.total + 255) / 256);
+      void *params[] = {L.args.data()};
+      cudaEventRecord(ev[2 * i], w->stream);
+      drv.launchKernel(d->kfun[L.loop], blocks, 1, 1, 256, 1, 1, 0, (CUstream)w->stream, params, nullptr);
+      cudaEventRecord(ev[2 * i + 1], w->stream);
+    }
+    cudaStreamSynchronize(w->stream);
+    for (size_t i = 0; i < d->log.size(); ++i) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]);
+      sum[d->log[i].loop] += t;
+      cnt[d->log[i].loop] += 1;
+    }
+  }
+  for (int l = 0; l < n_loops; ++l) kernel_ms[l] = cnt[l] ? sum[l] / cnt[l] : 0.0;
+  for (auto &e : ev) cudaEventDestroy(e);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  d->log.clear();
   return 0;
 }
 

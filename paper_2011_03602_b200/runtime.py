@@ -46,7 +46,8 @@ class Result(ctypes.Structure):
                 ("planned_bytes", ctypes.c_uint64), ("elided_bytes", ctypes.c_uint64),
                 ("unplanned_bytes", ctypes.c_uint64), ("block_bytes", ctypes.c_uint64),
                 ("epilogue_bytes", ctypes.c_uint64), ("directive_execs", ctypes.c_uint64),
-                ("launches", ctypes.c_uint64), ("stale_reads", ctypes.c_uint64), ("diag", ctypes.c_char * 256)]
+                ("launches", ctypes.c_uint64), ("stale_reads", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
+                ("d2h_bytes", ctypes.c_uint64), ("diag", ctypes.c_char * 256)]
 
     def to_dict(self) -> dict:
         return {
@@ -63,6 +64,8 @@ class Result(ctypes.Structure):
             "directive_execs": self.directive_execs,
             "launches": self.launches,
             "stale_reads": self.stale_reads,
+            "h2d_bytes": self.h2d_bytes,
+            "d2h_bytes": self.d2h_bytes,
             "diag": self.diag.decode(errors="replace"),
         }
 
@@ -102,6 +105,9 @@ def lib() -> ctypes.CDLL:
             "b2o_gemm_f32": ([ctypes.c_void_p] * 3 + [ctypes.c_int64] * 3 + [ctypes.c_void_p], ctypes.c_int),
             "b2o_fft2d_c64": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p], ctypes.c_int),
             "b2o_gemm_impl": ([], ctypes.c_int),
+            "b2o_bench_replay": ([ctypes.c_uint64, ctypes.c_int32, ctypes.POINTER(Pattern), ctypes.c_int32,
+                                  ctypes.c_int32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.c_int32, u64p], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -187,12 +193,10 @@ class NativeApp:
         check(lib().b2o_app_read(self.handle, worker, vid, out.ctypes.data, out.nbytes), "b2o_app_read")
         return out
 
-    def run(self, patterns: list[dict]) -> list[dict]:
-        """Execute pattern dicts {gpu_roots, directives, mode, repeats,
-        timeout_s, priority, device}; returns result dicts in order."""
+    def _patterns(self, patterns: list[dict]):
         n = len(patterns)
         keep = []
-        arr = (Pattern * n)()
+        arr = (Pattern * max(n, 1))()
         for i, p in enumerate(patterns):
             roots = (ctypes.c_uint8 * max(self.n_loops, 1))()
             for r in p.get("gpu_roots", ()):
@@ -209,12 +213,31 @@ class NativeApp:
                              ctypes.cast(darr, ctypes.POINTER(Directive)), float(p.get("priority", 0.0)),
                              float(p.get("timeout_s", 0.0) or 0.0), int(p.get("device", -1)),
                              MODE[p.get("mode", "coherent")], int(p.get("repeats", 1)), 0)
+        return arr, keep
+
+    def run(self, patterns: list[dict]) -> list[dict]:
+        """Execute pattern dicts {gpu_roots, directives, mode, repeats,
+        timeout_s, priority, device}; returns result dicts in order."""
+        n = len(patterns)
+        arr, _keep = self._patterns(patterns)
         L = lib()
         b = ctypes.c_uint64()
         check(L.b2o_submit(self.handle, arr, n, ctypes.byref(b)), "b2o_submit")
         res = (Result * max(n, 1))()
         check(L.b2o_wait(b.value, res, n, 0.0), "b2o_wait")
         return [res[i].to_dict() for i in range(n)]
+
+    def bench_replay(self, pattern: dict, warmup: int, steps: int, worker: int = 0) -> dict:
+        """Device-resident replay of the pattern's kernel launches (see
+        b2o_bench_replay in include/b2o.h)."""
+        arr, _keep = self._patterns([pattern])
+        ms = ctypes.c_double()
+        kms = (ctypes.c_double * max(self.n_loops, 1))()
+        nl = ctypes.c_uint64()
+        check(lib().b2o_bench_replay(self.handle, worker, arr, warmup, steps, ctypes.byref(ms), kms, self.n_loops,
+                                     ctypes.byref(nl)), "b2o_bench_replay")
+        return {"ms_per_step": ms.value, "kernel_ms": {i: kms[i] for i in range(self.n_loops) if kms[i] > 0},
+                "launches_per_step": nl.value}
 
     def close(self) -> None:
         if self.handle:
