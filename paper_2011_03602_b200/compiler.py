@@ -42,9 +42,10 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-6"
+COMPILER_VERSION = "b2o-compiler-8"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
+STENCIL_TILE = (32, 8)      # (k, j) tile of the 2.5-D stencil kernels
 
 _lock = threading.Lock()
 
@@ -141,6 +142,115 @@ class NestPlan:
     scalar_args: list[int]  # scalars passed by value
     swrites: list[int]      # scalars stored as lastprivate in the slab (incl. chain indices)
     locals_: list[int]      # scalars living in thread-local registers (non-chain)
+    shape: str = "flat"     # flat | stencil
+    ppt: int = 1            # points per thread (flat kernels)
+    staged: dict = None     # stencil kernels: var -> {ci, cj, dmin, planes}
+    streams: dict = None    # stencil kernels: var -> {ci, base}: one affine read per point
+
+
+def affine(e, idx_vars):
+    """(coefficients {var: c}, constant) when ``e`` is an integer affine form
+    of ``idx_vars`` with literal coefficients, else None."""
+    k = e[0]
+    if k == "num":
+        return None if e[2] else ({}, int(e[1]))
+    if k == "var":
+        return ({e[1]: 1}, 0) if e[1] in idx_vars else None
+    if k != "bin":
+        return None
+    a, b = affine(e[2], idx_vars), affine(e[3], idx_vars)
+    if a is None or b is None:
+        return None
+    op = e[1]
+    if op in "+-":
+        sg = 1 if op == "+" else -1
+        co = dict(a[0])
+        for v, c in b[0].items():
+            co[v] = co.get(v, 0) + sg * c
+        return ({v: c for v, c in co.items() if c}, a[1] + sg * b[1])
+    if op == "*":
+        if not a[0]:
+            return ({v: c * a[1] for v, c in b[0].items() if c * a[1]}, a[1] * b[1])
+        if not b[0]:
+            return ({v: c * b[1] for v, c in a[0].items() if c * b[1]}, a[1] * b[1])
+    return None
+
+
+def stencil_offset(e, iv, ci, cj):
+    """(di, dj, dk) of an index expression ``ci*i + cj*j + k + const`` with
+    every component in [-1, 1], or None."""
+    aff = affine(e, set(iv))
+    if aff is None:
+        return None
+    co, const = aff
+    if co != {iv[0]: ci, iv[1]: cj, iv[2]: 1}:
+        return None
+    hits = [(di, dj, dk) for di in (-1, 0, 1) for dj in (-1, 0, 1) for dk in (-1, 0, 1)
+            if di * ci + dj * cj + dk == const]
+    return hits[0] if len(hits) == 1 else None
+
+
+def _array_refs(e, out):
+    if e[0] == "arr":
+        out.append(e)
+        _array_refs(e[2], out)
+    elif e[0] == "bin":
+        _array_refs(e[2], out)
+        _array_refs(e[3], out)
+
+
+def _choose_shape(prog: Program, chain: list[int], writes: set[int], enable_stencil: bool = True):
+    """Kernel shape for a chain: the 2.5-D stencil template when a read-only
+    array is read at >= 4 distinct unit-radius offsets of a 3-deep affine
+    nest; otherwise a flat kernel with 1-4 points per thread depending on the
+    body's memory-reference count."""
+    if not chain:
+        return "flat", 1, None, None
+    body = prog.regions[prog.loops[chain[-1]].body].statements
+    if any(st.kind != "assign" for st in body):
+        return "flat", 1, None, None
+    refs: list = []
+    for st in body:
+        _array_refs(st.value, refs)
+        if st.target[0] == "arr":
+            refs.append(st.target)
+            _array_refs(st.target[2], refs)
+    staged = {}
+    by_var: dict[int, list] = {}
+    if len(chain) == 3:
+        iv = [prog.loops[c].index_var for c in chain]
+        for r in refs:
+            by_var.setdefault(r[1], []).append(r)
+        for v, rs in by_var.items():
+            if v in writes:
+                continue
+            aff = affine(rs[0][2], set(iv))
+            if aff is None:
+                continue
+            co = aff[0]
+            ci, cj = co.get(iv[0], 0), co.get(iv[1], 0)
+            if co.get(iv[2]) != 1 or cj < 3 or ci < 3 * cj:
+                continue
+            offs = [stencil_offset(r[2], iv, ci, cj) for r in rs]
+            if any(o is None for o in offs) or len(set(offs)) < 4:
+                continue
+            dis = [o[0] for o in offs]
+            staged[v] = {"ci": ci, "cj": cj, "dmin": min(dis), "planes": max(dis) - min(dis) + 1}
+    if staged and enable_stencil:
+        streams = {}
+        for v, rs in by_var.items():
+            if v in writes or v in staged:
+                continue
+            idx = {json.dumps(r[2]) for r in rs}
+            aff = affine(rs[0][2], set(iv))
+            if len(idx) != 1 or aff is None or aff[0].get(iv[2]) != 1 or set(aff[0]) - set(iv):
+                continue
+            co, const = aff
+            base = f"(int64_t){co.get(iv[1], 0)} * v{iv[1]} + v{iv[2]} + ({const})"
+            streams[v] = {"ci": co.get(iv[0], 0), "base": base}
+        return "stencil", 1, staged, streams
+    n = len(refs)
+    return "flat", (4 if n <= 4 else 2 if n <= 8 else 1), None, None
 
 
 def _first_access_is_read(prog: Program, lid: int, vid: int) -> bool:
@@ -174,7 +284,7 @@ def _first_access_is_read(prog: Program, lid: int, vid: int) -> bool:
     return bool(loop_first(lid))
 
 
-def plan_nest(prog: Program, lid: int) -> NestPlan:
+def plan_nest(prog: Program, lid: int, enable_stencil: bool = False) -> NestPlan:
     loop = prog.loops[lid]
     nest_loops = prog.subtree_loops(lid)
     reads, writes = prog.subtree_access(lid)
@@ -226,8 +336,9 @@ def plan_nest(prog: Program, lid: int) -> NestPlan:
     # roots evaluate chain bounds on the host: those reads are host-side
     need = set(scalar_args) | {a for a in arrays if a in reads} | bound_scalars
     swrites = sorted(set(chain_idx) | {v for v in locals_ if v in writes})
+    shape, ppt, staged, streams = _choose_shape(prog, chain, writes, enable_stencil)
     return NestPlan(lid, f"b2o_k{lid}", None, chain, sorted(need), sorted(writes), arrays,
-                    scalar_args, swrites, locals_)
+                    scalar_args, swrites, locals_, shape, ppt, staged, streams)
 
 
 # ---------------------------------------------------------------------------
@@ -245,7 +356,12 @@ class _Gen:
         self.blocks: list[dict] = []
         self.block_ids: dict[int, int] = {}
         self.calls: dict[int, dict] = {}
-        self.nests = {l.id: plan_nest(prog, l.id) for l in prog.loops}
+        self.nests = {l.id: plan_nest(prog, l.id, spec.get("stencil", False)) for l in prog.loops}
+        if spec.get("flat_ppt"):
+            for nst in self.nests.values():
+                if nst.shape == "flat" and nst.chain and all(
+                        st.kind == "assign" for st in prog.regions[prog.loops[nst.chain[-1]].body].statements):
+                    nst.ppt = int(spec["flat_ppt"])
         self.device_op = {}
         for l in prog.loops:
             self.device_op[l.id] = any(st.kind == "replaced" for st in prog.walk(l.body))
@@ -442,23 +558,21 @@ class _Gen:
 
     def kernel_struct(self, n: NestPlan) -> list[str]:
         D = max(len(n.chain), 1)
-        out = [f"typedef struct {{", "  uint32_t total;",
+        out = [f"typedef struct {{", "  uint32_t total, chunk;",
                f"  uint32_t n[{D}], mul[{D}], shr[{D}];", f"  int32_t lo[{D}];", "  void *slab;"]
-        reads = set(n.reads)
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
             out.append(f"  {const}{self.T(v)} *p{v};")
         for v in n.scalar_args:
             out.append(f"  {self.T(v)} s{v};")
         out.append(f"}} KA_L{n.root};")
-        del reads
         return out
 
     def launch_fn(self, n: NestPlan) -> list[str]:
         prog = self.prog
         lid = n.root
         out = [f"static void launch_L{lid}(b2o_exec *ex) {{", f"  ex->pre_launch(ex, {lid}); if (ex->stop) return;",
-               f"  KA_L{lid} a; memset(&a, 0, sizeof a);", "  uint64_t total = 1;"]
+               f"  KA_L{lid} a; memset(&a, 0, sizeof a);", "  uint64_t total = 1;", "  uint32_t geom[6];"]
         for d, c in enumerate(n.chain):
             cl = prog.loops[c]
             out.append(f"  {{ int32_t lo = {self.bound(cl.lower, self.host_name)}; "
@@ -480,19 +594,57 @@ class _Gen:
             out.append(f"  a.p{v} = ({const}{self.T(v)} *)ex->dev[{v}];")
         for v in n.scalar_args:
             out.append(f"  a.s{v} = S{v};")
-        out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, a.total);")
+        if n.shape == "stencil":
+            tk, tj = STENCIL_TILE
+            out.append(f"  {{ uint32_t tx = (a.n[2] + {tk - 1}) / {tk}, ty = (a.n[1] + {tj - 1}) / {tj};")
+            out.append(f"    uint64_t want = (uint64_t)B2O_TARGET_CTAS; uint64_t tiles = (uint64_t)tx * ty;")
+            out.append("    uint32_t chunks = (uint32_t)((want + tiles - 1) / tiles); if (chunks < 1) chunks = 1;")
+            out.append("    if (chunks > a.n[0]) chunks = a.n[0];")
+            out.append("    a.chunk = (a.n[0] + chunks - 1) / chunks;")
+            out.append(f"    geom[0] = tx; geom[1] = ty; geom[2] = (a.n[0] + a.chunk - 1) / a.chunk; "
+                       f"geom[3] = {tk}; geom[4] = {tj}; geom[5] = 1; }}")
+        else:
+            per = BLOCK_THREADS * n.ppt
+            out.append(f"  {{ uint64_t g = (total + {per - 1}) / {per}; geom[0] = (uint32_t)(g > 0x7fffffffu ? "
+                       f"0x7fffffffu : g); geom[1] = geom[2] = 1; geom[3] = {BLOCK_THREADS}; geom[4] = geom[5] = 1; }}")
+        out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, geom);")
         out.append("}")
         return out
 
+    def _finals(self, n: NestPlan, ind: str) -> list[str]:
+        prog = self.prog
+        chain_idx = [prog.loops[c].index_var for c in n.chain]
+        out = []
+        for v in n.swrites:
+            if v in chain_idx:
+                d = chain_idx.index(v)
+                val = f"a.lo[{d}] + (int32_t)a.n[{d}]"
+            else:
+                val = f"v{v}"
+            out.append(f"{ind}*({self.T(v)} *)((char *)a.slab + 8 * {v}) = {val};")
+        return out
+
+    def _locals(self, n: NestPlan, ind: str) -> list[str]:
+        out = []
+        for v in n.locals_:
+            init = f"a.s{v}" if v in n.scalar_args else "0"
+            cq = "const " if v not in n.writes else ""
+            out.append(f"{ind}{cq}{self.T(v)} v{v} = {init};")
+        return out
+
     def kernel_fn(self, n: NestPlan) -> list[str]:
+        if n.shape == "stencil":
+            return self.stencil_kernel_fn(n)
         prog = self.prog
         lid = n.root
-        out = [f'extern "C" __global__ void __launch_bounds__({BLOCK_THREADS}) {n.kernel}(const KA_L{lid} a) {{']
+        U = n.ppt
+        minb = self.spec.get("flat_min_blocks")
+        lb = f"{BLOCK_THREADS}, {int(minb)}" if minb else f"{BLOCK_THREADS}"
+        out = [f'extern "C" __global__ void __launch_bounds__({lb}) {n.kernel}(const KA_L{lid} a) {{']
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
             out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
-        out.append("  const uint32_t stride = gridDim.x * blockDim.x;")
-        out.append("  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {")
+        out.append("  auto point = [&](const uint32_t t) {")
         D = len(n.chain)
         for c in n.chain:
             out.append(f"    int32_t v{prog.loops[c].index_var}_;")
@@ -506,10 +658,7 @@ class _Gen:
         for c in n.chain:
             iv = prog.loops[c].index_var
             out.append(f"    const int32_t v{iv} = v{iv}_;")
-        for v in n.locals_:
-            init = f"a.s{v}" if v in n.scalar_args else "0"
-            cq = "const " if v not in n.writes else ""
-            out.append(f"    {cq}{self.T(v)} v{v} = {init};")
+        out.extend(self._locals(n, "    "))
         body: list[str] = []
         if D:
             self.dev_region(prog.loops[n.chain[-1]].body, 2, body)
@@ -517,20 +666,161 @@ class _Gen:
             self.dev_loop(lid, 2, body)
         out.extend(body)
         out.append("    if (t == a.total - 1u) {")
-        for v in n.swrites:
-            if v in [prog.loops[c].index_var for c in n.chain]:
-                d = [prog.loops[c].index_var for c in n.chain].index(v)
-                val = f"a.lo[{d}] + (int32_t)a.n[{d}]"
-            else:
-                val = f"v{v}"
-            out.append(f"      *({self.T(v)} *)((char *)a.slab + 8 * {v}) = {val};")
+        out.extend(self._finals(n, "      "))
         out.append("    }")
         for v in n.locals_:
             if v not in n.swrites:
                 out.append(f"    (void)v{v};")
+        out.append("  };")
+        out.append(f"  const uint32_t stride = gridDim.x * blockDim.x * {U}u;")
+        out.append(f"  for (uint32_t t0 = blockIdx.x * blockDim.x * {U}u + threadIdx.x; t0 < a.total; t0 += stride) {{")
+        if U > 1:
+            # whole group in range: unrolled straight-line points (loads of
+            # later points can issue before earlier stores: restrict pointers)
+            out.append(f"    if (t0 + {U - 1}u * blockDim.x < a.total) {{")
+            out.append("#pragma unroll")
+            out.append(f"      for (uint32_t u = 0; u < {U}u; ++u) point(t0 + u * blockDim.x);")
+            out.append("    } else {")
+            out.append(f"      for (uint32_t u = 0; u < {U}u && t0 + u * blockDim.x < a.total; ++u) point(t0 + u * blockDim.x);")
+            out.append("    }")
+        else:
+            out.append("    point(t0);")
         out.append("  }")
         out.append("}")
         return out
+
+    def stencil_kernel_fn(self, n: NestPlan) -> list[str]:
+        """2.5-D plane marching (SURVEY.md §2.2 K1 technique notes).
+
+        The CTA owns a TK x TJ tile of the two inner chain loops and walks a
+        chunk of the outer loop.  Staged arrays (read-only, >= 4 unit-radius
+        affine offsets) keep a rolling window of planes (tile + halo) in
+        shared memory: each element is read from HBM once, neighbours come
+        from SMEM.  Stream arrays (read-only, one affine index) are read
+        straight into registers.  Both are double-buffered in registers: the
+        next plane's halo values and stream values are requested before the
+        barrier of the current plane, so every thread keeps ~one plane of
+        loads in flight across the barriers."""
+        prog = self.prog
+        lid = n.root
+        tk, tj = STENCIL_TILE
+        hk, hj = tk + 2, tj + 2
+        nthr = tk * tj
+        halo = hk * hj
+        per = (halo + nthr - 1) // nthr  # halo elements per thread
+        iv = [prog.loops[c].index_var for c in n.chain]
+        minb = self.spec.get("stencil_min_blocks")
+        lb = f"{nthr}, {int(minb)}" if minb else f"{nthr}"
+        out = [f'extern "C" __global__ void __launch_bounds__({lb}) {n.kernel}(const KA_L{lid} a) {{']
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        for v, st in n.staged.items():
+            out.append(f"  __shared__ {self.T(v)} s{v}[{st['planes']}][{hj}][{hk}];")
+        out.append("  const int tk = threadIdx.x, tj = threadIdx.y;")
+        out.append(f"  const uint32_t ok_ = blockIdx.x * {tk}u + tk, oj_ = blockIdx.y * {tj}u + tj;")
+        out.append("  const bool inside = ok_ < a.n[2] && oj_ < a.n[1];")
+        out.append(f"  const int32_t v{iv[2]} = a.lo[2] + (int32_t)ok_;")
+        out.append(f"  const int32_t v{iv[1]} = a.lo[1] + (int32_t)oj_;")
+        out.append("  const int32_t i_begin = a.lo[0] + (int32_t)(blockIdx.z * a.chunk);")
+        out.append("  int32_t i_end = i_begin + (int32_t)a.chunk;")
+        out.append("  if (i_end > a.lo[0] + (int32_t)a.n[0]) i_end = a.lo[0] + (int32_t)a.n[0];")
+        out.append(f"  const int32_t j0 = a.lo[1] + (int32_t)(blockIdx.y * {tj}u) - 1;")
+        out.append(f"  const int32_t k0 = a.lo[2] + (int32_t)(blockIdx.x * {tk}u) - 1;")
+        out.append(f"  const int lin = tj * {tk} + tk;")
+        # halo slots owned by this thread
+        for q in range(per):
+            out.append(f"  const int hj{q} = (lin + {q * nthr}) / {hk}, hk{q} = (lin + {q * nthr}) - hj{q} * {hk};")
+            out.append(f"  const bool hv{q} = lin + {q * nthr} < {halo};")
+        for v, st in n.staged.items():
+            T = self.T(v)
+            L = prog.vars[v].length
+            ci, cj = st["ci"], st["cj"]
+            P, dmin = st["planes"], st["dmin"]
+            dmax = dmin + P - 1
+            out.append(f"  auto fetch{v} = [&](int32_t ii, int q_j, int q_k) -> {T} {{")
+            out.append(f"    const int64_t g = (int64_t){ci} * ii + (int64_t){cj} * (j0 + q_j) + (k0 + q_k);")
+            out.append(f"    return (g >= 0 && g < {L}) ? v{v}[g] : ({T})0;")
+            out.append("  };")
+            out.append(f"  auto bufof{v} = [&](int32_t q) -> int {{ return (int)((((int64_t)q - ({dmin})) % {P} + {P}) % {P}); }};")
+            out.append(f"  for (int32_t d = {dmin}; d < {dmax}; ++d) {{")
+            for q in range(per):
+                out.append(f"    if (hv{q}) s{v}[bufof{v}(i_begin + d)][hj{q}][hk{q}] = fetch{v}(i_begin + d, hj{q}, hk{q});")
+            out.append("  }")
+            for q in range(per):
+                out.append(f"  {T} h{v}_{q} = hv{q} ? fetch{v}(i_begin + {dmax}, hj{q}, hk{q}) : ({T})0;")
+        for v, st in n.streams.items():
+            T = self.T(v)
+            co, c0 = st["ci"], st["base"]
+            out.append(f"  const int64_t sb{v} = {c0};")
+            out.append(f"  {T} pf{v} = (inside && i_begin < i_end) ? v{v}[sb{v} + (int64_t){co} * i_begin] : ({T})0;")
+        out.append(f"  for (int32_t v{iv[0]} = i_begin; v{iv[0]} < i_end; ++v{iv[0]}) {{")
+        out.append(f"    const bool more = v{iv[0]} + 1 < i_end;")
+        for v, st in n.staged.items():
+            T = self.T(v)
+            dmax = st["dmin"] + st["planes"] - 1
+            out.append(f"    {{ const int b = bufof{v}(v{iv[0]} + {dmax});")
+            for q in range(per):
+                out.append(f"      if (hv{q}) s{v}[b][hj{q}][hk{q}] = h{v}_{q};")
+            out.append("    }")
+            out.append("    if (more) {")
+            for q in range(per):
+                out.append(f"      if (hv{q}) h{v}_{q} = fetch{v}(v{iv[0]} + {dmax + 1}, hj{q}, hk{q});")
+            out.append("    }")
+            out.append(f"    const int b{v}_base = bufof{v}(v{iv[0]});")
+        for v, st in n.streams.items():
+            T = self.T(v)
+            out.append(f"    const {T} c{v} = pf{v};")
+            out.append(f"    if (inside && more) pf{v} = v{v}[sb{v} + (int64_t){st['ci']} * (v{iv[0]} + 1)];")
+        out.append("    __syncthreads();")
+        out.append("    if (inside) {")
+        out.extend(self._locals(n, "      "))
+        body: list[str] = []
+        self._staged = n.staged
+        self._streams = n.streams
+        self._stencil_iv = iv
+        self.dev_region(prog.loops[n.chain[-1]].body, 3, body)
+        self._staged = None
+        self._streams = None
+        out.extend(body)
+        out.append(f"      if (v{iv[0]} == a.lo[0] + (int32_t)a.n[0] - 1 && ok_ == a.n[2] - 1u && oj_ == a.n[1] - 1u) {{")
+        out.extend(self._finals(n, "        "))
+        out.append("      }")
+        for v in n.locals_:
+            if v not in n.swrites:
+                out.append(f"      (void)v{v};")
+        out.append("    }")
+        out.append("    __syncthreads();")
+        out.append("  }")
+        out.append("}")
+        return out
+
+    def dev_name(self, vid: int, is_array: bool) -> str:
+        return f"v{vid}"
+
+    def dev_expr(self, e) -> str:
+        """Device rendering; staged stencil reads become shared-memory reads."""
+        staged = getattr(self, "_staged", None)
+        if not staged:
+            return render(e, self.local_name)
+
+        def rec(x):
+            k = x[0]
+            if k == "arr" and x[1] in staged:
+                st = staged[x[1]]
+                di, dj, dk = stencil_offset(x[2], self._stencil_iv, st["ci"], st["cj"])
+                P = st["planes"]
+                buf = f"((b{x[1]}_base + {di % P}) % {P})"
+                return f"s{x[1]}[{buf}][tj + {1 + dj}][tk + {1 + dk}]"
+            if k == "arr" and self._streams and x[1] in self._streams:
+                return f"c{x[1]}"
+            if k == "num" or k == "var":
+                return render(x, self.local_name)
+            if k == "arr":
+                return f"v{x[1]}[{rec(x[2])}]"
+            return f"({rec(x[2])} {x[1]} {rec(x[3])})"
+
+        return rec(e)
 
     def dev_loop(self, lid: int, ind: int, out: list[str]) -> None:
         loop = self.prog.loops[lid]
@@ -548,7 +838,7 @@ class _Gen:
                 if st.init is not None:
                     out.append(pad + f"v{st.var} = {render(st.init, self.local_name)};")
             elif st.kind == "assign":
-                out.append(pad + f"{render(st.target, self.local_name)} = {render(st.value, self.local_name)};")
+                out.append(pad + f"{self.dev_expr(st.target)} = {self.dev_expr(st.value)};")
             elif st.kind == "loop":
                 self.dev_loop(st.loop, ind, out)
             elif st.kind == "call":
@@ -691,7 +981,8 @@ class CompiledApp:
 
 
 def _spec_key(spec: dict) -> dict:
-    return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad")}
+    return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
+                                     "stencil_min_blocks", "flat_ppt", "flat_min_blocks")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

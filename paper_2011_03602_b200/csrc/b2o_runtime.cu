@@ -98,7 +98,7 @@ struct AppDev {
   struct Launch {
     int loop;
     std::vector<char> args;
-    uint32_t total;
+    uint32_t geom[6];
   };
   std::vector<Launch> log;
 };
@@ -304,19 +304,20 @@ void cb_pre_launch(b2o_exec *ex, int32_t loop) {
   }
 }
 
-void cb_launch(b2o_exec *ex, int32_t loop, void *args, uint32_t args_bytes, uint32_t total) {
+void cb_launch(b2o_exec *ex, int32_t loop, void *args, uint32_t args_bytes, const uint32_t *geom) {
   AppDev *d = D(ex);
-  if (args == nullptr || total == 0) {
+  if (args == nullptr || geom == nullptr) {
     set_error(d, B2O_RUNTIME_ERROR, "loop " + std::to_string(loop) + ": iteration space exceeds 2^32");
     return;
   }
-  (void)args_bytes;
-  const uint32_t threads = 256;
-  uint32_t blocks = (uint32_t)std::min<uint64_t>(((uint64_t)total + threads - 1) / threads, 0x7fffffffu);
   void *params[] = {args};
-  if (d->recording) d->log.push_back({loop, std::vector<char>((char *)args, (char *)args + args_bytes), total});
-  if (!cu_ok(d, drv.launchKernel(d->kfun[loop], blocks, 1, 1, threads, 1, 1, 0, (CUstream)d->w->stream, params,
-                               nullptr),
+  if (d->recording) {
+    AppDev::Launch L{loop, std::vector<char>((char *)args, (char *)args + args_bytes), {}};
+    std::copy(geom, geom + 6, L.geom);
+    d->log.push_back(std::move(L));
+  }
+  if (!cu_ok(d, drv.launchKernel(d->kfun[loop], geom[0], geom[1], geom[2], geom[3], geom[4], geom[5], 0,
+                               (CUstream)d->w->stream, params, nullptr),
              "cuLaunchKernel"))
     return;
   d->acc.launches++;
@@ -1002,11 +1003,9 @@ int b2o_bench_replay(uint64_t app, int32_t worker, const b2o_pattern *pattern, i
   if (d->log.empty()) return fail("pattern launches no kernel");
   auto replay = [&]() -> bool {
     for (auto &L : d->log) {
-      const uint32_t threads = 256;
-      uint32_t blocks = (uint32_t)(((uint64_t)L.total + threads - 1) / threads);
       void *params[] = {L.args.data()};
-      if (drv.launchKernel(d->kfun[L.loop], blocks, 1, 1, threads, 1, 1, 0, (CUstream)w->stream, params,
-                           nullptr) != CUDA_SUCCESS)
+      if (drv.launchKernel(d->kfun[L.loop], L.geom[0], L.geom[1], L.geom[2], L.geom[3], L.geom[4], L.geom[5], 0,
+                           (CUstream)w->stream, params, nullptr) != CUDA_SUCCESS)
         return false;
     }
     return true;
@@ -1025,31 +1024,34 @@ int b2o_bench_replay(uint64_t app, int32_t worker, const b2o_pattern *pattern, i
   cudaEventElapsedTime(&ms, e0, e1);
   *ms_per_step = steps > 0 ? ms / steps : 0.0;
   *launches_per_step = d->log.size();
-  // per-launch device time, one event pair per launch
-  std::vector<cudaEvent_t> ev(2 * d->log.size());
-  for (auto &e : ev) cudaEventCreate(&e);
+  // per-kernel device time: that loop's recorded launches back to back,
+  // one event pair around `passes` repetitions
   std::vector<double> sum(n_loops, 0.0);
   std::vector<int> cnt(n_loops, 0);
-  int passes = std::max(1, std::min(steps, 5));
-  for (int pss = 0; pss < passes; ++pss) {
-    for (size_t i = 0; i < d->log.size(); ++i) {
-      auto &L = d->log[i];
-      uint32_t blocks = (uint32_t)(((uint64_t)L.total + 255) / 256);
-      void *params[] = {L.args.data()};
-      cudaEventRecord(ev[2 * i], w->stream);
-      drv.launchKernel(d->kfun[L.loop], blocks, 1, 1, 256, 1, 1, 0, (CUstream)w->stream, params, nullptr);
-      cudaEventRecord(ev[2 * i + 1], w->stream);
-    }
-    cudaStreamSynchronize(w->stream);
-    for (size_t i = 0; i < d->log.size(); ++i) {
-      float t = 0.f;
-      cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]);
-      sum[d->log[i].loop] += t;
-      cnt[d->log[i].loop] += 1;
-    }
+  int passes = std::max(3, std::min(steps, 20));
+  for (int l = 0; l < n_loops; ++l) {
+    std::vector<const AppDev::Launch *> mine;
+    for (auto &L : d->log)
+      if (L.loop == l) mine.push_back(&L);
+    if (mine.empty()) continue;
+    auto issue = [&]() {
+      for (const AppDev::Launch *L : mine) {
+        void *params[] = {(void *)L->args.data()};
+        drv.launchKernel(d->kfun[l], L->geom[0], L->geom[1], L->geom[2], L->geom[3], L->geom[4], L->geom[5], 0,
+                         (CUstream)w->stream, params, nullptr);
+      }
+    };
+    issue();
+    cudaEventRecord(e0, w->stream);
+    for (int pss = 0; pss < passes; ++pss) issue();
+    cudaEventRecord(e1, w->stream);
+    cudaEventSynchronize(e1);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    sum[l] = t;
+    cnt[l] = passes * (int)mine.size();
   }
   for (int l = 0; l < n_loops; ++l) kernel_ms[l] = cnt[l] ? sum[l] / cnt[l] : 0.0;
-  for (auto &e : ev) cudaEventDestroy(e);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   d->log.clear();

@@ -1,0 +1,213 @@
+"""Batched and sharded GA drivers.
+
+``run_search_batched`` is the reference GA (``run_search``, src/ga.py:246-285)
+with one change: each generation's not-yet-cached genomes are measured in ONE
+``evaluator.measure_batch`` call (all B200 workers in parallel, or all ranks of
+a process group) instead of one ``measure`` at a time (src/ga.py:270).  The
+operators, the RNG stream, the memo semantics, the cache-hit count, the
+history and the final selection are the reference's own, so with a
+deterministic evaluator the ``SearchResult`` is identical to ``run_search``'s
+(tests/test_search.py).  SPEC.md:286 allows exactly this ("results are merged
+in genome order so outcomes are independent of completion order").
+
+``ShardedEvaluator`` spreads a batch over the ranks of a ``torch.distributed``
+process group (gloo, host-side results only: fitness units are independent,
+so there is no data-path collective): requests are assigned longest-predicted
+first (the reference cost model, src/evaluators.py:74-109) to the least
+loaded rank, each rank measures its share on its own B200, and the results
+are all-gathered so every rank continues with the same cache.
+"""
+
+from __future__ import annotations
+
+from .evaluator import _result_cls
+
+
+def _ga():
+    import gpuoffload.ga as ga  # the reference GA (operators, dataclasses)
+
+    return ga
+
+
+class _BatchRunner:
+    """GenomeEvaluator (src/ga.py:85-134) with batch submission."""
+
+    def __init__(self, model, space, evaluator, backend, on_evaluation):
+        ga = _ga()
+        from gpuoffload.evaluators import EvaluationRequest
+        from gpuoffload.model import ModelIndex, ReplacedBlock
+
+        self._Request = EvaluationRequest
+        self.ga = ga
+        self.model = model
+        self.space = space
+        self.evaluator = evaluator
+        self.backend = backend
+        self.on_evaluation = on_evaluation
+        self.index = ModelIndex(model)
+        self.cache: dict = {}
+        self.evaluations = 0
+        self.cache_hits = 0
+        self.replaced_blocks = tuple(st for _, _, st in model.walk_statements() if isinstance(st, ReplacedBlock))
+        self._needs_code = getattr(evaluator, "needs_code", True)
+
+    def _request(self, bits, tags):
+        from gpuoffload.codegen import emit_annotated
+        from gpuoffload.patterns import pattern_from_genome
+        from gpuoffload.transfers import plan_transfers
+
+        pattern = pattern_from_genome(self.model, self.space, bits)
+        plan = plan_transfers(self.model, pattern, self.index)
+        code = emit_annotated(self.model, pattern, plan, self.backend) if self._needs_code else ""
+        return self._Request(model=self.model, pattern=pattern, transfer_plan=plan, emitted_code=code,
+                             backend=self.backend, replaced_blocks=self.replaced_blocks, tags=dict(tags))
+
+    def evaluate_population(self, population, tags) -> list:
+        """Fitness of every individual, in population order.  First
+        occurrences of uncached genomes are measured together; repeats (in
+        this generation or earlier) are cache hits, exactly as the serial
+        loop counts them."""
+        ga = self.ga
+        fresh: list[tuple] = []
+        seen = set()
+        for bits in population:
+            bits = tuple(bits)
+            if bits not in self.cache and bits not in seen:
+                seen.add(bits)
+                fresh.append(bits)
+        requests = [self._request(b, tags) for b in fresh]
+        if requests:
+            measure_batch = getattr(self.evaluator, "measure_batch", None)
+            if measure_batch is not None:
+                results = measure_batch(requests)
+            else:
+                results = [self.evaluator.measure(r) for r in requests]
+        else:
+            results = []
+        fresh_res = {}
+        for bits, req, res in zip(fresh, requests, results):
+            fresh_res[bits] = (req, res)
+        out = []
+        for bits in population:
+            bits = tuple(bits)
+            if bits in self.cache:
+                self.cache_hits += 1
+                out.append(self.cache[bits])
+                continue
+            req, res = fresh_res[bits]
+            fit = ga.Fitness(res.time_seconds, res.evaluator_id)
+            self.cache[bits] = fit
+            self.evaluations += 1
+            if self.on_evaluation is not None:
+                self.on_evaluation(bits, req, res)
+            out.append(fit)
+        return out
+
+
+def run_search_batched(model, verdicts, evaluator, params, backend: str = "c_openacc", on_evaluation=None):
+    """``run_search`` (src/ga.py:246-285) with per-generation batch measurement."""
+    ga = _ga()
+    from gpuoffload.patterns import PatternError, build_genome_space
+
+    space = build_genome_space(model, verdicts)
+    if space.is_empty:
+        raise PatternError("no offloadable loops; skip the search and use the CPU-only pattern")
+    runner = _BatchRunner(model, space, evaluator, backend, on_evaluation)
+    import random
+
+    if space.length <= 2:
+        fits = runner.evaluate_population(list(space.all_genomes()), {"generation": 0})
+        history = (ga._generation_stats(0, fits, runner.evaluations),)
+    else:
+        rng = random.Random(params.seed)
+        population = ga.init_population(space.length, params, rng)
+        hist = []
+        for gen in range(params.generations):
+            fits = runner.evaluate_population(population, {"generation": gen})
+            hist.append(ga._generation_stats(gen, fits, runner.evaluations))
+            if gen + 1 < params.generations:
+                population = ga.next_generation(population, fits, params, rng)
+        history = tuple(hist)
+    best_bits, best_time, no_offload = ga._best_of_cache(runner.cache, space.length)
+    return ga.SearchResult(best_genome=best_bits, best_time=best_time, no_offload=no_offload,
+                           evaluations_performed=runner.evaluations, cache_hits=runner.cache_hits,
+                           history=history, genome_length=space.length)
+
+
+def exhaustive_search_batched(model, verdicts, evaluator, cap: int = 14, backend: str = "c_openacc",
+                              on_evaluation=None):
+    """``exhaustive_search`` (src/ga.py:292-321): all 2^a genomes in one batch."""
+    ga = _ga()
+    from gpuoffload.patterns import PatternError, build_genome_space
+
+    space = build_genome_space(model, verdicts)
+    if space.is_empty:
+        raise PatternError("no offloadable loops; nothing to enumerate")
+    if space.length > cap:
+        raise ga.ExhaustiveCapError(f"genome length {space.length} exceeds the exhaustive cap of {cap}")
+    runner = _BatchRunner(model, space, evaluator, backend, on_evaluation)
+    fits = runner.evaluate_population(list(space.all_genomes()), {"generation": 0})
+    history = (ga._generation_stats(0, fits, runner.evaluations),)
+    best_bits, best_time, no_offload = ga._best_of_cache(runner.cache, space.length)
+    return ga.SearchResult(best_genome=best_bits, best_time=best_time, no_offload=no_offload,
+                           evaluations_performed=runner.evaluations, cache_hits=runner.cache_hits,
+                           history=history, genome_length=space.length)
+
+
+def _predicted_cost(request) -> float:
+    try:
+        from gpuoffload.evaluators import CostModelParams, cost_model_time
+
+        r = cost_model_time(request, CostModelParams())
+        return r.time_seconds if r.time_seconds is not None else 0.0
+    except ImportError:
+        return 0.0
+
+
+def lpt_assignment(costs: list[float], workers: int) -> list[int]:
+    """Longest-processing-time-first: worker index per item (deterministic:
+    ties by item order, then lowest worker index)."""
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    load = [0.0] * workers
+    owner = [0] * len(costs)
+    for i in order:
+        w = min(range(workers), key=lambda k: (load[k], k))
+        owner[i] = w
+        load[w] += max(costs[i], 1e-12)
+    return owner
+
+
+class ShardedEvaluator:
+    """Evaluator protocol over a process group: ``measure_batch`` shards the
+    batch across ranks (one B200 each) and all-gathers the results."""
+
+    def __init__(self, inner, group=None):
+        import torch.distributed as dist
+
+        self.inner = inner
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.evaluator_id = getattr(inner, "evaluator_id", "sharded")
+        self.concurrency_safe = True
+        self.needs_code = getattr(inner, "needs_code", True)
+
+    def measure(self, request):
+        return self.measure_batch([request])[0]
+
+    def measure_batch(self, requests) -> list:
+        owner = lpt_assignment([_predicted_cost(r) for r in requests], self.world)
+        mine = [i for i, o in enumerate(owner) if o == self.rank]
+        inner_batch = getattr(self.inner, "measure_batch", None)
+        reqs = [requests[i] for i in mine]
+        res = inner_batch(reqs) if inner_batch else [self.inner.measure(r) for r in reqs]
+        local = [(i, r.time_seconds, r.validity, r.evaluator_id, r.diagnostics) for i, r in zip(mine, res)]
+        gathered: list = [None] * self.world
+        self.dist.all_gather_object(gathered, local, group=self.group)
+        cls = _result_cls()
+        out: list = [None] * len(requests)
+        for part in gathered:
+            for i, t, validity, eid, diag in part:
+                out[i] = cls(t, validity, eid, diag)
+        return out
