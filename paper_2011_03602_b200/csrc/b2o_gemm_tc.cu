@@ -1,6 +1,373 @@
-// b2o_gemm_tc.cu — placeholder until the tcgen05/TMEM 3xTF32 GEMM lands.
+// b2o_gemm_tc.cu — the cublas_gemm replacement on 5th-generation tensor
+// cores: C = A B, fp32 in / fp32 out, computed as 3xTF32
+//
+//     A B ~= Ah Bh + Ah Bl + Al Bh,   Xh = rna_tf32(X),  Xl = rna_tf32(X - Xh)
+//
+// so the result carries ~fp32 accuracy (plain TF32 would
+// give ~5e-4 per product).
+//
+// Kernel anatomy (sm_100a, one CTA per 128 x 256 output tile):
+//   warp 0      TMA producer: Ah, Al (128 x 32) and BhT, BlT (256 x 32) per
+//               K-block, 128-byte swizzle, into a STAGES-deep smem ring
+//               (mbarrier full/empty pairs, expect_tx byte counts);
+//   warp 1      TMEM allocation (2 x 256 columns) + the single elected MMA
+//               issuer: per K-block 4 k-steps x 3 tcgen05.mma.kind::tf32
+//               (M=128, N=256, K=8); tcgen05.commit frees the smem stage;
+//               every KCHUNK of K goes to one of two ping-pong TMEM
+//               accumulators, whose completion is committed to the epilogue;
+//   warps 2..9  epilogue: drain each finished chunk accumulator with
+//               tcgen05.ld 32x32b.x32 (warp w owns TMEM lane quarter w%4 and
+//               one 128-column half) and add it to fp32 running sums in
+//               registers (round-to-nearest), release the accumulator, and
+//               finally store the tile with 128-bit global stores.
+// Draining every 128 of K keeps the tensor core's own accumulation short:
+// the error no longer grows with K (1e-5 at K=1024 single-accumulator vs
+// ~1e-6 chunked, tests/test_ops_gpu.py).
+// A preparation kernel splits A (row-major, K-major already) and splits +
+// transposes B so both operands are K-major (the canonical UMMA layout).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
 #include <cstdint>
-extern "C" int b2o_gemm_tc_f32(const float *, const float *, float *, int64_t, int64_t, int64_t, void *) {
-  return -2;
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
+constexpr int A_TILE = BM * BK * 4;                 // 16 KB
+constexpr int B_TILE = BN * BK * 4;                 // 32 KB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;  // 96 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr uint32_t TMEM_COLS = 512;  // two 256-column fp32 accumulators
+constexpr int KCHUNK_BLOCKS = 4;     // 4 x BK = 128 of K per accumulator fill
+
+// instruction descriptor: D f32 (bits 4-5 = 1), A/B tf32 (bits 7-9, 10-12 =
+// 2), both K-major, N>>3 at bits 17-22, M>>4 at bits 24-28
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
-extern "C" int b2o_gemm_impl(void) { return 0; }
+
+// shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B
+// apart (SBO), version 1 (sm_100)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// operand preparation: hi/lo split (A), split + transpose (B)
+// ---------------------------------------------------------------------------
+
+__global__ void split_kernel(const float *__restrict__ x, float *__restrict__ hi, float *__restrict__ lo, size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    float v = x[i];
+    float h = __uint_as_float(tf32_rna(v));
+    hi[i] = h;
+    lo[i] = __uint_as_float(tf32_rna(v - h));
+  }
+}
+
+// B is K x N row-major; write BhT/BlT as N x K row-major (K-major operand)
+__global__ void split_transpose_kernel(const float *__restrict__ b, float *__restrict__ hiT, float *__restrict__ loT,
+                                       int K, int N) {
+  __shared__ float tile[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) tile[r][threadIdx.x] = b[(size_t)(k0 + r) * N + n0 + threadIdx.x];
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    float v = tile[threadIdx.x][r];
+    float h = __uint_as_float(tf32_rna(v));
+    size_t o = (size_t)(n0 + r) * K + k0 + threadIdx.x;
+    hiT[o] = h;
+    loT[o] = __uint_as_float(tf32_rna(v - h));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the GEMM kernel
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                   const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                   float *__restrict__ C, int M, int N, int K) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+  // bars: full[STAGES], empty[STAGES], acc_full[2], acc_empty[2]; then the TMEM slot
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * STAGES + 4);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+  const uint32_t accf0 = smem_u32(bars + 2 * STAGES), acce0 = smem_u32(bars + 2 * STAGES + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // tile raster: consecutive CTAs share the same B panel (N tile) column
+  const int tiles_m = M / BM;
+  const int m0 = (blockIdx.x % tiles_m) * BM;
+  const int n0 = (blockIdx.x / tiles_m) * BN;
+  const int kblocks = K / BK;
+  const int nchunks = (kblocks + KCHUNK_BLOCKS - 1) / KCHUNK_BLOCKS;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mAh) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mBh) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(empty0 + 8 * s, ph ^ 1);
+        uint8_t *st = smem + s * STAGE_BYTES;
+        const uint32_t fb = full0 + 8 * s;
+        mbar_expect_tx(fb, STAGE_BYTES);
+        tma_load_2d(smem_u32(st), &mAh, kb * BK, m0, fb);
+        tma_load_2d(smem_u32(st + A_TILE), &mAl, kb * BK, m0, fb);
+        tma_load_2d(smem_u32(st + 2 * A_TILE), &mBh, kb * BK, n0, fb);
+        tma_load_2d(smem_u32(st + 2 * A_TILE + B_TILE), &mBl, kb * BK, n0, fb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c >= 2) mbar_wait(acce0 + 8 * buf, ((c - 2) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc_tmem = tmem + (uint32_t)(buf * BN);
+        const int kb_end = min(kblocks, (c + 1) * KCHUNK_BLOCKS);
+        for (int kb = c * KCHUNK_BLOCKS; kb < kb_end; ++kb) {
+          const int s = kb % STAGES;
+          const uint32_t ph = (kb / STAGES) & 1;
+          mbar_wait(full0 + 8 * s, ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a_h = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t a_l = a_h + A_TILE;
+          const uint32_t b_h = a_h + 2 * A_TILE;
+          const uint32_t b_l = b_h + B_TILE;
+          const bool first_kb = kb == c * KCHUNK_BLOCKS;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t off = kk * 8 * 4;  // 8 tf32 = 32 bytes along K inside the swizzle atom
+            const uint32_t acc = (first_kb && kk == 0) ? 0u : 1u;
+            umma_tf32(acc_tmem, smem_desc(a_l + off), smem_desc(b_h + off), acc);
+            umma_tf32(acc_tmem, smem_desc(a_h + off), smem_desc(b_l + off), 1u);
+            umma_tf32(acc_tmem, smem_desc(a_h + off), smem_desc(b_h + off), 1u);
+          }
+          umma_commit(empty0 + 8 * s);
+        }
+        umma_commit(accf0 + 8 * buf);
+      }
+    }
+  } else {
+    // epilogue warps 2..9: TMEM lane quarter = warp % 4, column half h
+    const int q = warp % 4;
+    const int h = (warp - 2) / 4;
+    float sum[128];
+#pragma unroll
+    for (int j = 0; j < 128; ++j) sum[j] = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      mbar_wait(accf0 + 8 * buf, (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int part = 0; part < 4; ++part) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + part * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+              "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum[part * 32 + j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce0 + 8 * buf) : "memory");
+    }
+    const int row = m0 + q * 32 + lane;
+    float4 *dst = (float4 *)(C + (size_t)row * N + n0 + h * 128);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dst[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess) fn = (EncodeFn)p;
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap *m, const float *base, int rows, int cols, int box_rows) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct Workspace {
+  float *p = nullptr;
+  size_t bytes = 0;
+};
+std::mutex ws_mu;
+std::map<int, Workspace> ws_by_dev;
+
+float *workspace(size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(ws_mu);
+  Workspace &w = ws_by_dev[dev];
+  if (w.bytes < bytes) {
+    if (w.p) cudaFree(w.p);
+    w.p = nullptr;
+    w.bytes = 0;
+    if (cudaMalloc(&w.p, bytes) != cudaSuccess) return nullptr;
+    w.bytes = bytes;
+  }
+  return w.p;
+}
+
+}  // namespace
+
+extern "C" int b2o_gemm_impl(void) { return 1; }
+
+// returns -2 when the shape does not tile (caller falls back to SIMT)
+extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t m, int64_t n, int64_t k,
+                               void *stream) {
+  if (m % BM || n % BN || k % BK || m <= 0 || n <= 0 || k <= 0 || m > (1 << 20) || n > (1 << 20) ||
+      k > (1 << 20) || (n % 32) || (k % 32))
+    return -2;
+  if (!encode_fn()) return -2;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t a_elems = (size_t)m * k, b_elems = (size_t)n * k;
+  float *ws = workspace(sizeof(float) * 2 * (a_elems + b_elems));
+  if (!ws) return -1;
+  float *Ah = ws, *Al = ws + a_elems, *Bh = Al + a_elems, *Bl = Bh + b_elems;
+  split_kernel<<<148 * 8, 256, 0, s>>>(A, Ah, Al, a_elems);
+  dim3 tg((unsigned)(n / 32), (unsigned)(k / 32));
+  split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bh, Bl, (int)k, (int)n);
+  CUtensorMap mAh, mAl, mBh, mBl;
+  if (!make_map(&mAh, Ah, (int)m, (int)k, BM) || !make_map(&mAl, Al, (int)m, (int)k, BM) ||
+      !make_map(&mBh, Bh, (int)n, (int)k, BN) || !make_map(&mBl, Bl, (int)n, (int)k, BN))
+    return -1;
+  static bool attr[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+      return -1;
+    attr[dev & 63] = true;
+  }
+  const unsigned tiles = (unsigned)((m / BM) * (n / BN));
+  gemm_tc_kernel<<<tiles, THREADS, SMEM_BYTES, s>>>(mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
