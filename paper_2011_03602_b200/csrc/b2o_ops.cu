@@ -169,18 +169,138 @@ __global__ void __launch_bounds__(kFftThreads) fft_cols_kernel(float2 *__restric
   }
 }
 
+// ---- radix-16 path (N = 16^P): digit-reversed load, in-place DIT passes,
+// each thread owns whole 16-point groups in registers ----------------------
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// 16-point DFT of v[0..15] in registers (natural order in, natural order out)
+__device__ __forceinline__ void dft16(float2 (&v)[16]) {
+  // radix-2 DIF stages with the 16th roots of unity, then bit-reverse
+  const float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f, r2 = 0.70710678118654752f;
+  const float2 w[8] = {{1.f, 0.f}, {c1, -s1}, {r2, -r2}, {s1, -c1}, {0.f, -1.f}, {-s1, -c1}, {-r2, -r2}, {-c1, -s1}};
+#pragma unroll
+  for (int span = 8, step = 1; span >= 1; span >>= 1, step <<= 1) {
+#pragma unroll
+    for (int base = 0; base < 16; base += 2 * span) {
+#pragma unroll
+      for (int k = 0; k < span; ++k) {
+        float2 a = v[base + k], b = v[base + k + span];
+        v[base + k] = make_float2(a.x + b.x, a.y + b.y);
+        v[base + k + span] = cmul(make_float2(a.x - b.x, a.y - b.y), w[k * step]);
+      }
+    }
+  }
+  // outputs are bit-reversed: swap into natural order
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = ((i & 1) << 3) | ((i & 2) << 1) | ((i & 4) >> 1) | ((i & 8) >> 3);
+    if (r > i) {
+      float2 t = v[i];
+      v[i] = v[r];
+      v[r] = t;
+    }
+  }
+}
+
+// shared-memory swizzle: XOR the low nibble of the float2 index with the
+// next nibble, so every pass of the Stockham radix-16 FFT below (reads at
+// stride N/16, writes at stride L, plus the natural-order load/store) hits 16
+// distinct 8-byte bank pairs per half-warp
+__device__ __forceinline__ int sw16(int i) { return i ^ ((i >> 4) & 15); }
+
+// Stockham autosort radix-16 FFT (natural order in and out) over COUNT
+// sequences of length n = 16^digits, interleaved in shared memory: element i
+// of sequence c lives at s[sw16(i) * COUNT + c] (so COUNT adjacent columns of
+// a matrix are stored the way they arrive from global memory).  Each pass
+// reads a thread's 16-point groups into registers, barrier, writes them back:
+// in place without a second buffer.  Consecutive threads take consecutive
+// sequences of the same group (conflict-free), twiddles come from one table
+// load per group and a complex recurrence.  tw[m] = exp(-2 pi i m / n).
+template <int COUNT, int GROUPS_PER_THREAD>
+__device__ void smem_fft16(float2 *s, int n, int digits, const float2 *__restrict__ tw) {
+  const int stride_in = n / 16;
+  for (int p = 0, L = 1; p < digits; ++p, L *= 16) {
+    const int tw_scale = n / (16 * L);
+    float2 v[GROUPS_PER_THREAD][16];
+    int dst[GROUPS_PER_THREAD];
+#pragma unroll
+    for (int q = 0; q < GROUPS_PER_THREAD; ++q) {
+      const int g = threadIdx.x + q * blockDim.x;
+      const int c = g % COUNT;
+      const int gg = g / COUNT;  // = j * L + k
+      const int k = gg % L;
+      const int j = gg / L;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[q][r] = s[sw16(gg + r * stride_in) * COUNT + c];
+      if (p > 0 && k > 0) {
+        const float2 w1 = tw[(k * tw_scale) & (n - 1)];
+        float2 w = w1;
+#pragma unroll
+        for (int r = 1; r < 16; ++r) {
+          v[q][r] = cmul(v[q][r], w);
+          w = cmul(w, w1);
+        }
+      }
+      dft16(v[q]);
+      dst[q] = (j * 16 * L + k) * COUNT + c;  // element index * COUNT + c, before swizzle
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < GROUPS_PER_THREAD; ++q) {
+      const int c = dst[q] % COUNT;
+      const int e = dst[q] / COUNT;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) s[sw16(e + r * L) * COUNT + c] = v[q][r];
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int kColGroup16 = 2;  // 2 columns (64 KB smem): 3 CTAs per SM overlap load/compute/store
+
+__global__ void __launch_bounds__(256) fft16_rows_kernel(const float2 *__restrict__ x, float2 *__restrict__ y, int n,
+                                                         int digits, const float2 *__restrict__ tw) {
+  extern __shared__ float2 s[];
+  const size_t row = blockIdx.x;
+  const float2 *src = x + row * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s[sw16(i)] = src[i];
+  __syncthreads();
+  smem_fft16<1, 1>(s, n, digits, tw);
+  float2 *dst = y + row * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = s[sw16(i)];
+}
+
+__global__ void __launch_bounds__(512, 2) fft16_cols_kernel(float2 *__restrict__ y, int n, int digits,
+                                                         const float2 *__restrict__ tw) {
+  extern __shared__ float2 s[];
+  const int c0 = blockIdx.x * kColGroup16;
+  for (int idx = threadIdx.x; idx < n * kColGroup16; idx += blockDim.x) {
+    const int r = idx / kColGroup16, c = idx - r * kColGroup16;
+    s[sw16(r) * kColGroup16 + c] = y[(size_t)r * n + c0 + c];
+  }
+  __syncthreads();
+  smem_fft16<kColGroup16, 1>(s, n, digits, tw);
+  for (int idx = threadIdx.x; idx < n * kColGroup16; idx += blockDim.x) {
+    const int r = idx / kColGroup16, c = idx - r * kColGroup16;
+    y[(size_t)r * n + c0 + c] = s[sw16(r) * kColGroup16 + c];
+  }
+}
+
 std::mutex tw_mu;
 std::map<std::pair<int, int64_t>, float2 *> tw_cache;  // (device, n) -> table
 
-float2 *twiddles(int64_t n) {
+float2 *twiddles(int64_t n, bool full = false) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(tw_mu);
-  auto key = std::make_pair(dev, n);
+  auto key = std::make_pair(dev, full ? -n : n);
   auto it = tw_cache.find(key);
   if (it != tw_cache.end()) return it->second;
-  std::vector<float2> h(n / 2);
-  for (int64_t k = 0; k < n / 2; ++k) {
+  std::vector<float2> h(full ? n : n / 2);
+  for (int64_t k = 0; k < (int64_t)h.size(); ++k) {
     double a = -2.0 * M_PI * (double)k / (double)n;
     h[k] = make_float2((float)cos(a), (float)sin(a));
   }
@@ -195,6 +315,27 @@ float2 *twiddles(int64_t n) {
 
 extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) {
   if (n < 8 || n > 4096 || (n & (n - 1)) != 0 || n % kColGroup != 0) return -1;
+  int digits16 = 0;
+  for (int64_t m = 1; m < n; m *= 16) ++digits16;
+  if ((int64_t)1 << (4 * digits16) == n && n >= 256) {
+    float2 *tw = twiddles(n, true);
+    if (!tw) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    static bool attr16[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr16[dev & 63]) {
+      cudaFuncSetAttribute(fft16_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(fft16_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr16[dev & 63] = true;
+    }
+    if (n != 4096 && n != 256) return -1;
+    fft16_rows_kernel<<<(unsigned)n, (unsigned)(n / 16), sizeof(float2) * n, s>>>((const float2 *)x, (float2 *)y,
+                                                                             (int)n, digits16, tw);
+    fft16_cols_kernel<<<(unsigned)(n / kColGroup16), (unsigned)(n / 16 * kColGroup16), sizeof(float2) * n * kColGroup16, s>>>(
+        (float2 *)y, (int)n, digits16, tw);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   int logn = 0;
   while ((1 << logn) < n) ++logn;
   float2 *tw = twiddles(n);

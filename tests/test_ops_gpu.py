@@ -56,7 +56,7 @@ def test_simt_fallback_for_odd_shapes(torch_cuda):
     assert np.linalg.norm(c - ref) / np.linalg.norm(ref) < 1e-6
 
 
-@pytest.mark.parametrize("n", [8, 64, 1024, 4096])
+@pytest.mark.parametrize("n", [8, 64, 256, 1024, 4096])
 def test_fft2d_matches_numpy(torch_cuda, n):
     from paper_2011_03602_b200.runtime import lib
 
