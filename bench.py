@@ -253,6 +253,7 @@ def b200_arm(args, dist: Dist) -> None:
             r = ev.measure_payloads(g["doc"], [pat])[0]
             e2e.append((time.perf_counter() - t0, r))
         dist.barrier()
+    ga = ga_arm(args, dist) if args.ga else None
     ms = dist.max(rep["ms_per_step"])
     e2e_s = dist.max(statistics.median(t for t, _ in e2e))
     last = e2e[-1][1]
@@ -286,9 +287,44 @@ def b200_arm(args, dist: Dist) -> None:
                          "kind": "port", "sample": f"one full Himeno M app run ({nn} sweeps), C restatement "
                                                    "(oracle/cgen.py), gcc -O3 OpenMP, all-CPU genome"},
         "app_speedup_vs_cpu": round(cpu_s / e2e_s, 2),
+        "ga": ga,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
+
+
+def ga_arm(args, dist: Dist) -> dict | None:
+    """BASELINE config 5: the reference GA (pop 64 x 20 generations) on Himeno
+    L, each generation's uncached genomes measured in one batch; under
+    torchrun the batch is sharded LPT over the ranks (one B200 each) and the
+    results are all-gathered (search.ShardedEvaluator).  patterns/sec =
+    evaluations_performed / GA wall time (max over ranks)."""
+    try:
+        from gpuoffload.ga import GAParams
+        from gpuoffload.irdoc import load_ir_document
+        from gpuoffload.screen import screen_model
+    except ImportError as exc:
+        return {"skipped": f"reference package not importable: {exc}"}
+    from paper_2011_03602_b200.evaluator import B200Evaluator
+    from paper_2011_03602_b200.search import ShardedEvaluator, run_search_batched
+
+    g = golden(args.ga_workload)
+    model = load_ir_document(json.dumps(g["doc"]))
+    ev = B200Evaluator(g["spec"], devices=[dist.local_rank], timeout_seconds=args.ga_timeout)
+    ev.app_for(g["doc"])  # compile + load + all-CPU reference run, untimed
+    evaluator = ShardedEvaluator(ev) if dist.world > 1 else ev
+    params = GAParams(population_size=args.ga_pop, generations=args.ga_gens, seed=args.ga_seed)
+    dist.barrier()
+    t0 = time.perf_counter()
+    res = run_search_batched(model, screen_model(model), evaluator, params)
+    wall = dist.max(time.perf_counter() - t0)
+    valid = sum(1 for r in ev.log if r.get("validity") == "valid")
+    local = dist.sum(float(len(ev.log)))
+    return {"workload": f"{args.ga_workload} inline nn={sweeps_of(g['doc'])}, pop {args.ga_pop} x {args.ga_gens} gens",
+            "patterns_per_s": round(res.evaluations_performed / wall, 3), "evaluations": res.evaluations_performed,
+            "cache_hits": res.cache_hits, "wall_s": round(wall, 3), "best_genome": "".join(map(str, res.best_genome)),
+            "best_time_s": res.best_time, "measured_by_all_ranks": int(local), "valid_on_rank0": valid,
+            "history_evals": [h.evaluations for h in res.history][:6]}
 
 
 def main() -> None:
@@ -298,6 +334,12 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--ga", type=int, default=1, help="also measure GA patterns/sec (config 5)")
+    ap.add_argument("--ga-workload", default="himeno_L")
+    ap.add_argument("--ga-pop", type=int, default=64)
+    ap.add_argument("--ga-gens", type=int, default=20)
+    ap.add_argument("--ga-seed", type=int, default=20201106)
+    ap.add_argument("--ga-timeout", type=float, default=120.0)
     args = ap.parse_args()
     dist = Dist()
     try:

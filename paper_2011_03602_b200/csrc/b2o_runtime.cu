@@ -85,7 +85,7 @@ struct AppDev {
   void *cells = nullptr;     // pinned 8-byte scalar cells
   void *slab = nullptr;      // device scalar slab
   void *slab_init = nullptr; // pinned initial slab contents
-  std::vector<uint8_t> hv, dv, hmod, dev_dirty;
+  std::vector<uint8_t> hv, dv, hmod, dev_dirty, host_touched;
   std::vector<uint8_t> is_root, dev_inside, hook_mask;
   std::vector<std::vector<b2o_directive>> hooks[2];
   b2o_exec ex{};
@@ -235,6 +235,7 @@ void copy_d2h(AppDev *d, int v) {
   }
   cuda_ok(d, cudaStreamSynchronize(d->w->stream), "D2H sync");
   d->acc.d2h_bytes += var_bytes(d, v);
+  d->host_touched[v] = 1;
 }
 
 // make the host copy current (coherent mode)
@@ -287,6 +288,7 @@ void cb_host_access(b2o_exec *ex, int32_t set) {
     d->hv[v] = 1;
     d->dv[v] = 0;
     d->hmod[v] = 1;
+    d->host_touched[v] = 1;
   }
 }
 
@@ -416,6 +418,7 @@ void cb_external(b2o_exec *ex, int32_t call) {
   d->hv[op.out] = 1;
   d->dv[op.out] = 0;
   d->hmod[op.out] = 1;
+  d->host_touched[op.out] = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -496,6 +499,7 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
   d->dv.assign(nv, 0);
   d->hmod.assign(nv, 0);
   d->dev_dirty.assign(nv, 0);
+  d->host_touched.assign(nv, 0);
   d->is_root.assign(std::max(nl, 1), 0);
   d->dev_inside.assign(std::max(nl, 1), 0);
   d->hook_mask.assign(std::max(nl, 1), 0);
@@ -521,6 +525,19 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
   return 0;
 }
 
+void par_memcpy(void *dst, const void *src, size_t bytes) {
+  if (bytes < ((size_t)16 << 20)) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t chunk = (bytes + 7) / 8;
+#pragma omp parallel for num_threads(8) schedule(static)
+  for (int t = 0; t < 8; ++t) {
+    size_t off = (size_t)t * chunk;
+    if (off < bytes) memcpy((char *)dst + off, (const char *)src + off, std::min(chunk, bytes - off));
+  }
+}
+
 // restore pristine state; host copies valid, device copies "not present"
 void reset_state(AppDev *d) {
   const b2o_module_info *info = d->app->info;
@@ -528,13 +545,14 @@ void reset_state(AppDev *d) {
     const b2o_var_info &vi = info->vars[v];
     if (!vi.is_array) {
       memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
-    } else if (vi.written) {
-      memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
+    } else if (vi.written && d->host_touched[v]) {
+      par_memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
       if (d->dev_dirty[v])
         cudaMemcpyAsync(d->dev[v], d->dev_pristine[v], d->app->initial[v].size(), cudaMemcpyDeviceToDevice,
                         d->w->stream);
     }
     d->dev_dirty[v] = 0;
+    d->host_touched[v] = 0;
   }
   cudaMemcpyAsync(d->slab, d->slab_init, 8 * (size_t)std::max(info->n_vars, 1), cudaMemcpyHostToDevice,
                   d->w->stream);
@@ -602,8 +620,10 @@ void compare_outputs(AppDev *d, b2o_result &r) {
     };
     uint64_t nbad = 0;
     double w = 0.0;
+    const int nthr = n > (1 << 20) ? 8 : 1;
     if (oi.mode == B2O_CMP_NORMWISE) {
       double num = 0.0, den = 0.0;
+#pragma omp parallel for num_threads(nthr) reduction(+ : num, den) schedule(static)
       for (int64_t i = 0; i < n; ++i) {
         double c = val(cand, i), rr = val(ref, i);
         num += (c - rr) * (c - rr);
@@ -613,13 +633,21 @@ void compare_outputs(AppDev *d, b2o_result &r) {
       if (!(rel <= oi.rel_tol)) nbad = 1;
       w = rel;
     } else {
+      const double tol = oi.rel_tol;
+      uint64_t cnt = 0;
+      double worst_local = 0.0;
+      bool saw_nan = false;
+#pragma omp parallel for num_threads(nthr) reduction(+ : cnt) reduction(max : worst_local) reduction(|| : saw_nan) schedule(static)
       for (int64_t i = 0; i < n; ++i) {
         double c = val(cand, i), rr = val(ref, i);
         double diff = std::fabs(c - rr);
-        if (!(diff <= std::max(oi.rel_tol * std::fabs(rr), 1e-12))) ++nbad;
+        if (!(diff <= std::max(tol * std::fabs(rr), 1e-12))) ++cnt;
         double rel = diff / std::max(std::fabs(rr), 1e-30);
-        if (rel > w || std::isnan(rel)) w = std::isnan(rel) ? INFINITY : rel;
+        if (std::isnan(rel)) saw_nan = true;
+        else if (rel > worst_local) worst_local = rel;
       }
+      nbad = cnt;
+      w = saw_nan ? INFINITY : worst_local;
     }
     worst = std::max(worst, w);
     if (nbad && first_bad.empty()) first_bad = vi.name;
