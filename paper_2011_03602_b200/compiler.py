@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-8"
+COMPILER_VERSION = "b2o-compiler-12"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 STENCIL_TILE = (32, 8)      # (k, j) tile of the 2.5-D stencil kernels
@@ -143,7 +143,8 @@ class NestPlan:
     swrites: list[int]      # scalars stored as lastprivate in the slab (incl. chain indices)
     locals_: list[int]      # scalars living in thread-local registers (non-chain)
     shape: str = "flat"     # flat | stencil
-    ppt: int = 1            # points per thread (flat kernels)
+    ppt: int = 1            # points per thread (flat kernels, strided by the block)
+    kb: int = 1             # consecutive innermost-index points per thread (flat kernels)
     staged: dict = None     # stencil kernels: var -> {ci, cj, dmin, planes}
     streams: dict = None    # stencil kernels: var -> {ci, base}: one affine read per point
 
@@ -249,8 +250,12 @@ def _choose_shape(prog: Program, chain: list[int], writes: set[int], enable_sten
             base = f"(int64_t){co.get(iv[1], 0)} * v{iv[1]} + v{iv[2]} + ({const})"
             streams[v] = {"ci": co.get(iv[0], 0), "base": base}
         return "stencil", 1, staged, streams
+    # points per thread (strided by the block: coalescing kept) amortise the
+    # per-thread prologue; keep refs x points within a ~96-value register
+    # budget (measured: NAS-MG resid 23 refs best at 4, Himeno Jacobi 34 refs
+    # at 2, tools/kernel_sweep.py)
     n = len(refs)
-    return "flat", (4 if n <= 4 else 2 if n <= 8 else 1), None, None
+    return "flat", max(1, min(4, 96 // max(n, 1))), None, None
 
 
 def _first_access_is_read(prog: Program, lid: int, vid: int) -> bool:
@@ -338,7 +343,7 @@ def plan_nest(prog: Program, lid: int, enable_stencil: bool = False) -> NestPlan
     swrites = sorted(set(chain_idx) | {v for v in locals_ if v in writes})
     shape, ppt, staged, streams = _choose_shape(prog, chain, writes, enable_stencil)
     return NestPlan(lid, f"b2o_k{lid}", None, chain, sorted(need), sorted(writes), arrays,
-                    scalar_args, swrites, locals_, shape, ppt, staged, streams)
+                    scalar_args, swrites, locals_, shape=shape, ppt=ppt, staged=staged, streams=streams)
 
 
 # ---------------------------------------------------------------------------
@@ -357,6 +362,10 @@ class _Gen:
         self.block_ids: dict[int, int] = {}
         self.calls: dict[int, dict] = {}
         self.nests = {l.id: plan_nest(prog, l.id, spec.get("stencil", False)) for l in prog.loops}
+        for nst in self.nests.values():
+            if nst.shape == "flat" and nst.chain and nst.ppt == 1 and all(
+                    st.kind == "assign" for st in prog.regions[prog.loops[nst.chain[-1]].body].statements):
+                nst.kb = int(spec.get("flat_kblock", 1))
         if spec.get("flat_ppt"):
             for nst in self.nests.values():
                 if nst.shape == "flat" and nst.chain and all(
@@ -559,7 +568,7 @@ class _Gen:
     def kernel_struct(self, n: NestPlan) -> list[str]:
         D = max(len(n.chain), 1)
         out = [f"typedef struct {{", "  uint32_t total, chunk;",
-               f"  uint32_t n[{D}], mul[{D}], shr[{D}];", f"  int32_t lo[{D}];", "  void *slab;"]
+               f"  uint32_t n[{D}], tn[{D}], mul[{D}], shr[{D}];", f"  int32_t lo[{D}];", "  void *slab;"]
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
             out.append(f"  {const}{self.T(v)} *p{v};")
@@ -585,9 +594,15 @@ class _Gen:
             out.append(f"    ex->host_access(ex, {sid}); if (ex->stop) return;")
             out.append(f"    fast_L{lid}(ex); return;")
             out.append("  }")
+            D = len(n.chain)
+            out.append(f"  for (int d = 0; d < {D}; ++d) a.tn[d] = a.n[d];")
+            if n.kb > 1:
+                out.append(f"  a.tn[{D - 1}] = (a.n[{D - 1}] + {n.kb - 1}) / {n.kb};")
+                out.append("  total = 1;")
+                out.append(f"  for (int d = 0; d < {D}; ++d) total *= a.tn[d];")
             out.append("  if (total > 0xFFFFFFFFull) { ex->launch(ex, %d, 0, 0, 0); return; }" % lid)
             for d in range(1, len(n.chain)):
-                out.append(f"  b2o_fastdiv_init(a.n[{d}], &a.mul[{d}], &a.shr[{d}]);")
+                out.append(f"  b2o_fastdiv_init(a.tn[{d}], &a.mul[{d}], &a.shr[{d}]);")
         out.append("  a.total = (uint32_t)total; a.slab = ex->slab;")
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
@@ -605,8 +620,9 @@ class _Gen:
                        f"geom[3] = {tk}; geom[4] = {tj}; geom[5] = 1; }}")
         else:
             per = BLOCK_THREADS * n.ppt
-            out.append(f"  {{ uint64_t g = (total + {per - 1}) / {per}; geom[0] = (uint32_t)(g > 0x7fffffffu ? "
-                       f"0x7fffffffu : g); geom[1] = geom[2] = 1; geom[3] = {BLOCK_THREADS}; geom[4] = geom[5] = 1; }}")
+            cap = int(self.spec.get("flat_grid_cap", 0)) or 0x7FFFFFFF
+            out.append(f"  {{ uint64_t g = (total + {per - 1}) / {per}; geom[0] = (uint32_t)(g > {cap}u ? "
+                       f"{cap}u : g); geom[1] = geom[2] = 1; geom[3] = {BLOCK_THREADS}; geom[4] = geom[5] = 1; }}")
         out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, geom);")
         out.append("}")
         return out
@@ -648,26 +664,53 @@ class _Gen:
         D = len(n.chain)
         for c in n.chain:
             out.append(f"    int32_t v{prog.loops[c].index_var}_;")
+        KB = n.kb
         if D:
             out.append("    uint32_t r = t;")
             for d in range(D - 1, 0, -1):
                 iv = prog.loops[n.chain[d]].index_var
                 out.append(f"    {{ uint32_t q = b2o_fastdiv(r, a.mul[{d}], a.shr[{d}]); "
-                           f"v{iv}_ = a.lo[{d}] + (int32_t)(r - q * a.n[{d}]); r = q; }}")
-            out.append(f"    v{prog.loops[n.chain[0]].index_var}_ = a.lo[0] + (int32_t)r;")
-        for c in n.chain:
+                           f"v{iv}_ = (int32_t)(r - q * a.tn[{d}]); r = q; }}")
+            out.append(f"    v{prog.loops[n.chain[0]].index_var}_ = (int32_t)r;")
+        for d, c in enumerate(n.chain):
             iv = prog.loops[c].index_var
-            out.append(f"    const int32_t v{iv} = v{iv}_;")
+            if d == D - 1 and KB > 1:
+                continue
+            out.append(f"    const int32_t v{iv} = a.lo[{d}] + v{iv}_;")
         out.extend(self._locals(n, "    "))
-        body: list[str] = []
-        if D:
-            self.dev_region(prog.loops[n.chain[-1]].body, 2, body)
+        if KB > 1:
+            # KB consecutive points of the innermost loop per thread: one scope
+            # per point with the same base pointers, so loads shared between
+            # neighbouring points are common subexpressions
+            kv = prog.loops[n.chain[-1]].index_var
+            out.append(f"    const int32_t kb0 = v{kv}_ * {KB};")
+            out.append("    const bool last_t = t == a.total - 1u;")
+            for guarded in (False, True):
+                out.append(f"    {'} else {' if guarded else f'if (kb0 + {KB} <= (int32_t)a.n[{D - 1}]) {{'}")
+                for u in range(KB):
+                    out.append(f"      {{ const int32_t v{kv} = a.lo[{D - 1}] + kb0 + {u};")
+                    if guarded:
+                        out.append(f"        if (kb0 + {u} < (int32_t)a.n[{D - 1}]) {{")
+                    body: list[str] = []
+                    self.dev_region(prog.loops[n.chain[-1]].body, 4, body)
+                    out.extend(body)
+                    out.append(f"        if (last_t && kb0 + {u} == (int32_t)a.n[{D - 1}] - 1) {{")
+                    out.extend(self._finals(n, "          "))
+                    out.append("        }")
+                    if guarded:
+                        out.append("        }")
+                    out.append("      }")
+            out.append("    }")
         else:
-            self.dev_loop(lid, 2, body)
-        out.extend(body)
-        out.append("    if (t == a.total - 1u) {")
-        out.extend(self._finals(n, "      "))
-        out.append("    }")
+            body: list[str] = []
+            if D:
+                self.dev_region(prog.loops[n.chain[-1]].body, 2, body)
+            else:
+                self.dev_loop(lid, 2, body)
+            out.extend(body)
+            out.append("    if (t == a.total - 1u) {")
+            out.extend(self._finals(n, "      "))
+            out.append("    }")
         for v in n.locals_:
             if v not in n.swrites:
                 out.append(f"    (void)v{v};")
@@ -742,11 +785,14 @@ class _Gen:
             out.append(f"    const int64_t g = (int64_t){ci} * ii + (int64_t){cj} * (j0 + q_j) + (k0 + q_k);")
             out.append(f"    return (g >= 0 && g < {L}) ? v{v}[g] : ({T})0;")
             out.append("  };")
-            out.append(f"  auto bufof{v} = [&](int32_t q) -> int {{ return (int)((((int64_t)q - ({dmin})) % {P} + {P}) % {P}); }};")
+            # plane i_begin + dmin lives in buffer 0, the next in 1, ...; the
+            # window rotates by one buffer per plane (no modulo in the loop)
             out.append(f"  for (int32_t d = {dmin}; d < {dmax}; ++d) {{")
             for q in range(per):
-                out.append(f"    if (hv{q}) s{v}[bufof{v}(i_begin + d)][hj{q}][hk{q}] = fetch{v}(i_begin + d, hj{q}, hk{q});")
+                out.append(f"    if (hv{q}) s{v}[d - ({dmin})][hj{q}][hk{q}] = fetch{v}(i_begin + d, hj{q}, hk{q});")
             out.append("  }")
+            out.append(f"  int b{v}_base = {-dmin};          // buffer of plane i (offset 0)")
+            out.append(f"  int b{v}_new = {P - 1};           // buffer receiving plane i + dmax")
             for q in range(per):
                 out.append(f"  {T} h{v}_{q} = hv{q} ? fetch{v}(i_begin + {dmax}, hj{q}, hk{q}) : ({T})0;")
         for v, st in n.streams.items():
@@ -759,15 +805,12 @@ class _Gen:
         for v, st in n.staged.items():
             T = self.T(v)
             dmax = st["dmin"] + st["planes"] - 1
-            out.append(f"    {{ const int b = bufof{v}(v{iv[0]} + {dmax});")
             for q in range(per):
-                out.append(f"      if (hv{q}) s{v}[b][hj{q}][hk{q}] = h{v}_{q};")
-            out.append("    }")
+                out.append(f"    if (hv{q}) s{v}[b{v}_new][hj{q}][hk{q}] = h{v}_{q};")
             out.append("    if (more) {")
             for q in range(per):
                 out.append(f"      if (hv{q}) h{v}_{q} = fetch{v}(v{iv[0]} + {dmax + 1}, hj{q}, hk{q});")
             out.append("    }")
-            out.append(f"    const int b{v}_base = bufof{v}(v{iv[0]});")
         for v, st in n.streams.items():
             T = self.T(v)
             out.append(f"    const {T} c{v} = pf{v};")
@@ -791,6 +834,10 @@ class _Gen:
                 out.append(f"      (void)v{v};")
         out.append("    }")
         out.append("    __syncthreads();")
+        for v, st in n.staged.items():
+            P = st["planes"]
+            out.append(f"    b{v}_base = b{v}_base + 1 == {P} ? 0 : b{v}_base + 1;")
+            out.append(f"    b{v}_new = b{v}_new + 1 == {P} ? 0 : b{v}_new + 1;")
         out.append("  }")
         out.append("}")
         return out
@@ -810,7 +857,7 @@ class _Gen:
                 st = staged[x[1]]
                 di, dj, dk = stencil_offset(x[2], self._stencil_iv, st["ci"], st["cj"])
                 P = st["planes"]
-                buf = f"((b{x[1]}_base + {di % P}) % {P})"
+                buf = f"((b{x[1]}_base + {di % P}) % {P})" if di else f"b{x[1]}_base"
                 return f"s{x[1]}[{buf}][tj + {1 + dj}][tk + {1 + dk}]"
             if k == "arr" and self._streams and x[1] in self._streams:
                 return f"c{x[1]}"
@@ -982,7 +1029,8 @@ class CompiledApp:
 
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
-                                     "stencil_min_blocks", "flat_ppt", "flat_min_blocks")}
+                                     "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
+                                     "flat_grid_cap")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

@@ -37,7 +37,7 @@ def test_chains_follow_the_screen():
 def test_kernel_shapes():
     prog = Program(golden("himeno_M")["doc"])
     jac, cpy = plan_nest(prog, 1), plan_nest(prog, 7)
-    assert jac.shape == "flat" and jac.ppt == 1
+    assert jac.shape == "flat" and jac.ppt == 2
     assert cpy.shape == "flat" and cpy.ppt == 4
     sten = plan_nest(prog, 1, enable_stencil=True)
     assert sten.shape == "stencil" and set(sten.staged) == {prog.var_by_name["p"].id}
