@@ -254,7 +254,7 @@ def _choose_shape(prog: Program, chain: list[int], writes: set[int], enable_sten
     # per-thread prologue; keep refs x points within a ~96-value register
     # budget (measured: NAS-MG resid 23 refs best at 4, Himeno Jacobi 34 refs
     # at 2, tools/kernel_sweep.py)
-    n = len(refs)
+    n = len({(r[1], json.dumps(r[2])) for r in refs})  # distinct memory references
     return "flat", max(1, min(4, 96 // max(n, 1))), None, None
 
 
