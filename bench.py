@@ -70,11 +70,21 @@ def sweeps_of(doc: dict) -> int:
 # ---------------------------------------------------------------------------
 
 
+def visible_gpus() -> int:
+    try:
+        out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=30).stdout
+        return max(1, sum(1 for ln in out.splitlines() if ln.startswith("GPU ")))
+    except (OSError, subprocess.SubprocessError):
+        return 1
+
+
 class Dist:
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        # one rank per GPU; more ranks than GPUs (testing on a 1-GPU box)
+        # share devices round-robin
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0")) % visible_gpus()
         self.pg = None
         if self.world > 1:
             import torch.distributed as dist
@@ -265,7 +275,9 @@ def b200_arm(args, dist: Dist) -> None:
     achieved = 60 * pts / (kms * 1e-3) / 1e9 if kms else None
     if dist.rank != 0:
         return
-    cpu_s, cores = cpu_run(g["doc"], g["spec"], openmp=True, runs=1)
+    # the CPU baseline is timed on rank 0 at N=1 only (other ranks would
+    # contend for the same host cores)
+    cpu_s, cores = cpu_run(g["doc"], g["spec"], openmp=True, runs=1) if dist.world == 1 else (None, None)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
@@ -285,8 +297,9 @@ def b200_arm(args, dist: Dist) -> None:
         "kernels_us": {f"b2o_k{k}": round(v * 1e3, 2) for k, v in rep["kernel_ms"].items()},
         "cpu_baseline": {"value": round(bytes_per_step / cpu_s / 1e9, 3), "unit": "GB/s", "cores": cores,
                          "kind": "port", "sample": f"one full Himeno M app run ({nn} sweeps), C restatement "
-                                                   "(oracle/cgen.py), gcc -O3 OpenMP, all-CPU genome"},
-        "app_speedup_vs_cpu": round(cpu_s / e2e_s, 2),
+                                                   "(oracle/cgen.py), gcc -O3 OpenMP, all-CPU genome"}
+        if cpu_s else None,
+        "app_speedup_vs_cpu": round(cpu_s / e2e_s, 2) if cpu_s else None,
         "ga": ga,
         "clocks": clk.summary(),
     }
