@@ -264,6 +264,7 @@ def b200_arm(args, dist: Dist) -> None:
             e2e.append((time.perf_counter() - t0, r))
         dist.barrier()
     ga = ga_arm(args, dist) if args.ga else None
+    ops = ops_arm(dist) if args.ops else None
     ms = dist.max(rep["ms_per_step"])
     e2e_s = dist.max(statistics.median(t for t, _ in e2e))
     last = e2e[-1][1]
@@ -301,6 +302,7 @@ def b200_arm(args, dist: Dist) -> None:
         if cpu_s else None,
         "app_speedup_vs_cpu": round(cpu_s / e2e_s, 2) if cpu_s else None,
         "ga": ga,
+        "ops": ops,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -340,6 +342,62 @@ def ga_arm(args, dist: Dist) -> dict | None:
             "history_evals": [h.evaluations for h in res.history][:6]}
 
 
+def ops_arm(dist: Dist) -> dict:
+    """BASELINE config 3 kernels on resident data: the tcgen05 3xTF32 GEMM
+    (cublas_gemm replacement) at 4096^3 and the radix-16 FFT (cufft_exec
+    replacement) at 4096^2, CUDA events on the launching stream."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2011_03602_b200.runtime import lib
+
+    try:
+        import torch
+    except ImportError:
+        return {"skipped": "torch unavailable for device buffers"}
+    dev = torch.device("cuda", dist.local_rank)
+    torch.cuda.set_device(dev)
+    L = lib()
+    st = torch.cuda.current_stream().cuda_stream
+    n = 4096
+    a, b = torch.rand(n, n, device=dev), torch.rand(n, n, device=dev)
+    c = torch.empty(n, n, device=dev)
+    x = torch.rand(2 * n * n, device=dev) * 2 - 1
+    y = torch.empty_like(x)
+
+    def timed(fn, iters=10):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    gemm_ms = timed(lambda: L.b2o_gemm_f32(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, n, n, st))
+    err = float(np.linalg.norm(c[:256].double().cpu().numpy() - (a[:256].double() @ b.double()).cpu().numpy())
+                / np.linalg.norm((a[:256].double() @ b.double()).cpu().numpy()))
+    fft_ms = timed(lambda: L.b2o_fft2d_c64(x.data_ptr(), y.data_ptr(), n, st))
+    pk = peaks()
+    tf32_peak = pk["bf16_tflops"] / 2  # dense TF32 = half the dense BF16 rate on the same tensor pipe
+    tf32_issued = 3 * 2 * n ** 3 / (gemm_ms * 1e-3) / 1e12
+    fft_gbs = 2 * 2 * 8 * n * n / (fft_ms * 1e-3) / 1e9
+    del ctypes
+    return {"gemm_4096_ms": round(gemm_ms, 4), "gemm_tflops_fp32_equiv": round(2 * n ** 3 / (gemm_ms * 1e-3) / 1e12, 1),
+            "gemm_tf32_tflops_issued": round(tf32_issued, 1),
+            "gemm_roofline": {"bound": "tensor", "achieved": round(tf32_issued, 1), "peak": round(tf32_peak, 1),
+                              "unit": "TFLOP/s", "frac": round(tf32_issued / tf32_peak, 3),
+                              "peak_source": "MEASURED_PEAKS bf16_tflops / 2 (dense TF32)"},
+            "gemm_normwise_err_rows0_255": err,
+            "fft_4096_ms": round(fft_ms, 4),
+            "fft_roofline": {"bound": "hbm", "achieved": round(fft_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                             "frac": round(fft_gbs / pk["hbm_gbs"], 3), "bytes": "2 passes x read+write complex64"}}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -348,6 +406,7 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--ga", type=int, default=1, help="also measure GA patterns/sec (config 5)")
+    ap.add_argument("--ops", type=int, default=1, help="also time the GEMM/FFT block kernels (config 3)")
     ap.add_argument("--ga-workload", default="himeno_L")
     ap.add_argument("--ga-pop", type=int, default=64)
     ap.add_argument("--ga-gens", type=int, default=20)

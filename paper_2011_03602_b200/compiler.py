@@ -42,10 +42,11 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-12"
+COMPILER_VERSION = "b2o-compiler-13"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 STENCIL_TILE = (32, 8)      # (k, j) tile of the 2.5-D stencil kernels
+BRICK_DEPTH = 4             # outer-loop points per thread in brick kernels
 
 _lock = threading.Lock()
 
@@ -237,6 +238,8 @@ def _choose_shape(prog: Program, chain: list[int], writes: set[int], enable_sten
                 continue
             dis = [o[0] for o in offs]
             staged[v] = {"ci": ci, "cj": cj, "dmin": min(dis), "planes": max(dis) - min(dis) + 1}
+    if staged and enable_stencil == "brick":
+        return "brick", 1, staged, None
     if staged and enable_stencil:
         streams = {}
         for v, rs in by_var.items():
@@ -609,7 +612,12 @@ class _Gen:
             out.append(f"  a.p{v} = ({const}{self.T(v)} *)ex->dev[{v}];")
         for v in n.scalar_args:
             out.append(f"  a.s{v} = S{v};")
-        if n.shape == "stencil":
+        if n.shape == "brick":
+            tk, tj = STENCIL_TILE
+            out.append(f"  geom[0] = (a.n[2] + {tk - 1}) / {tk}; geom[1] = (a.n[1] + {tj - 1}) / {tj}; "
+                       f"geom[2] = (a.n[0] + {BRICK_DEPTH - 1}) / {BRICK_DEPTH}; geom[3] = {tk}; geom[4] = {tj}; "
+                       "geom[5] = 1;")
+        elif n.shape == "stencil":
             tk, tj = STENCIL_TILE
             out.append(f"  {{ uint32_t tx = (a.n[2] + {tk - 1}) / {tk}, ty = (a.n[1] + {tj - 1}) / {tj};")
             out.append(f"    uint64_t want = (uint64_t)B2O_TARGET_CTAS; uint64_t tiles = (uint64_t)tx * ty;")
@@ -651,6 +659,8 @@ class _Gen:
     def kernel_fn(self, n: NestPlan) -> list[str]:
         if n.shape == "stencil":
             return self.stencil_kernel_fn(n)
+        if n.shape == "brick":
+            return self.brick_kernel_fn(n)
         prog = self.prog
         lid = n.root
         U = n.ppt
@@ -728,6 +738,67 @@ class _Gen:
             out.append("    }")
         else:
             out.append("    point(t0);")
+        out.append("  }")
+        out.append("}")
+        return out
+
+    def brick_kernel_fn(self, n: NestPlan) -> list[str]:
+        """3-D brick tiling: the CTA stages a (BI+2) x (TJ+2) x (TK+2) box of
+        each staged array (tile + one-point halo) in shared memory with ONE
+        barrier, then every thread computes BI points along the outer chain
+        loop, unrolled, so the stream loads of all BI points are independent
+        and in flight together.  Staged neighbours come from SMEM."""
+        prog = self.prog
+        lid = n.root
+        tk, tj = STENCIL_TILE
+        BI = BRICK_DEPTH
+        hk, hj, hi = tk + 2, tj + 2, BI + 2
+        nthr = tk * tj
+        iv = [prog.loops[c].index_var for c in n.chain]
+        out = [f'extern "C" __global__ void __launch_bounds__({nthr}) {n.kernel}(const KA_L{lid} a) {{']
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        for v in n.staged:
+            out.append(f"  __shared__ {self.T(v)} s{v}[{hi}][{hj}][{hk}];")
+        out.append("  const int tk = threadIdx.x, tj = threadIdx.y;")
+        out.append(f"  const uint32_t ok_ = blockIdx.x * {tk}u + tk, oj_ = blockIdx.y * {tj}u + tj;")
+        out.append("  const bool inside = ok_ < a.n[2] && oj_ < a.n[1];")
+        out.append(f"  const int32_t v{iv[2]} = a.lo[2] + (int32_t)ok_;")
+        out.append(f"  const int32_t v{iv[1]} = a.lo[1] + (int32_t)oj_;")
+        out.append(f"  const int32_t i0 = a.lo[0] + (int32_t)(blockIdx.z * {BI}u);")
+        out.append(f"  const int32_t i_end = a.lo[0] + (int32_t)a.n[0];")
+        out.append(f"  const int32_t j0 = a.lo[1] + (int32_t)(blockIdx.y * {tj}u) - 1;")
+        out.append(f"  const int32_t k0 = a.lo[2] + (int32_t)(blockIdx.x * {tk}u) - 1;")
+        out.append(f"  const int lin = tj * {tk} + tk;")
+        for v, st in n.staged.items():
+            T = self.T(v)
+            L = prog.vars[v].length
+            out.append(f"  for (int e = lin; e < {hi * hj * hk}; e += {nthr}) {{")
+            out.append(f"    const int ii = e / {hj * hk}, rem = e - ii * {hj * hk}, jj = rem / {hk}, kk = rem - jj * {hk};")
+            out.append(f"    const int64_t g = (int64_t){st['ci']} * (i0 - 1 + ii) + (int64_t){st['cj']} * (j0 + jj) + (k0 + kk);")
+            out.append(f"    s{v}[ii][jj][kk] = (g >= 0 && g < {L}) ? v{v}[g] : ({T})0;")
+            out.append("  }")
+        out.append("  __syncthreads();")
+        out.append("  if (!inside) return;")
+        out.append("#pragma unroll")
+        out.append(f"  for (int q = 0; q < {BI}; ++q) {{")
+        out.append(f"    const int32_t v{iv[0]} = i0 + q;")
+        out.append(f"    if (v{iv[0]} >= i_end) break;")
+        out.extend(self._locals(n, "    "))
+        body: list[str] = []
+        self._staged = {v: dict(st, brick=True) for v, st in n.staged.items()}
+        self._streams = None
+        self._stencil_iv = iv
+        self.dev_region(prog.loops[n.chain[-1]].body, 2, body)
+        self._staged = None
+        out.extend(body)
+        out.append(f"    if (v{iv[0]} == i_end - 1 && ok_ == a.n[2] - 1u && oj_ == a.n[1] - 1u) {{")
+        out.extend(self._finals(n, "      "))
+        out.append("    }")
+        for v in n.locals_:
+            if v not in n.swrites:
+                out.append(f"    (void)v{v};")
         out.append("  }")
         out.append("}")
         return out
@@ -856,6 +927,8 @@ class _Gen:
             if k == "arr" and x[1] in staged:
                 st = staged[x[1]]
                 di, dj, dk = stencil_offset(x[2], self._stencil_iv, st["ci"], st["cj"])
+                if st.get("brick"):
+                    return f"s{x[1]}[q + {1 + di}][tj + {1 + dj}][tk + {1 + dk}]"
                 P = st["planes"]
                 buf = f"((b{x[1]}_base + {di % P}) % {P})" if di else f"b{x[1]}_base"
                 return f"s{x[1]}[{buf}][tj + {1 + dj}][tk + {1 + dk}]"
