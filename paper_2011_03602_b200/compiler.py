@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-13"
+COMPILER_VERSION = "b2o-compiler-14"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 STENCIL_TILE = (32, 8)      # (k, j) tile of the 2.5-D stencil kernels
@@ -148,6 +148,7 @@ class NestPlan:
     kb: int = 1             # consecutive innermost-index points per thread (flat kernels)
     staged: dict = None     # stencil kernels: var -> {ci, cj, dmin, planes}
     streams: dict = None    # stencil kernels: var -> {ci, base}: one affine read per point
+    quad: dict = None       # quad kernels: quad_plan() result
 
 
 def affine(e, idx_vars):
@@ -259,6 +260,78 @@ def _choose_shape(prog: Program, chain: list[int], writes: set[int], enable_sten
     # at 2, tools/kernel_sweep.py)
     n = len({(r[1], json.dumps(r[2])) for r in refs})  # distinct memory references
     return "flat", max(1, min(4, 96 // max(n, 1))), None, None
+
+
+QUAD = 4  # points per thread of the vectorised flat kernel (16-byte chunks of 4-byte elements)
+
+
+def quad_plan(prog: Program, chain: list[int], precision: str) -> dict | None:
+    """Vectorised ("quad") flat kernel eligibility (SURVEY.md §7 "Alignment":
+    odd row pitches forbid aligned 3-D tiles, so process the flattened index
+    space in aligned 16-byte chunks plus neighbour offsets).
+
+    Eligible when the chain body is straight-line array assignments whose
+    every array reference is ``sum_d c_d * i_d + k + const`` with literal
+    coefficients, coefficient 1 on the innermost chain index ``k``, the same
+    outer coefficients ``c_d`` for every reference (one row function
+    ``F = sum c_d i_d``), 4-byte elements, and no array both read and written
+    in the body (each written at a single offset).  A thread then owns one
+    16-byte-aligned quad of a row (an array both read and written is allowed
+    when every reference uses the write's offset): every reference ``const`` maps lane ``u``
+    to element ``b + const + u`` of an aligned chunk known at compile time.
+    Returns ``{"outer": (c_d...), "reads": {(v, const)}, "writes": {v: const}}``
+    or None."""
+    if not chain:
+        return None
+    body = prog.regions[prog.loops[chain[-1]].body].statements
+    if not body or any(st.kind != "assign" or st.target[0] != "arr" for st in body):
+        return None
+    iv = [prog.loops[c].index_var for c in chain]
+    # int scalars the body reads (by value, never written in a straight-line
+    # array body) may appear in index expressions as well: they are part of
+    # the row function, e.g. i and j of a k-rooted Himeno nest
+    extra = set()
+    for st in body:
+        extra |= {v for v in expr_vars(st.value) + expr_vars(st.target[2])
+                  if not prog.vars[v].is_array and prog.vars[v].base_type == "int" and v not in iv}
+    ovars = iv[:-1] + sorted(extra)
+    ivs = set(iv) | extra
+    outer = None
+    reads, writes = set(), {}
+
+    def ref(r):
+        nonlocal outer
+        if ctype(prog, r[1], precision) not in ("float", "int32_t"):
+            return None
+        aff = affine(r[2], ivs)
+        if aff is None or aff[0].get(iv[-1]) != 1:
+            return None
+        o = tuple(aff[0].get(v, 0) for v in ovars)
+        if outer is None:
+            outer = o
+        elif o != outer:
+            return None
+        return aff[1]
+
+    for st in body:
+        refs: list = []
+        _array_refs(st.value, refs)
+        _array_refs(st.target[2], refs)
+        for r in refs:
+            c = ref(r)
+            if c is None:
+                return None
+            reads.add((r[1], c))
+        c = ref(st.target)
+        if c is None or writes.get(st.target[1], c) != c:
+            return None
+        writes[st.target[1]] = c
+    # an array both read and written must be touched at one offset only
+    # (point-local read-modify-write); reads after the write in body order
+    # then see the new lane value (quad_kernel_fn)
+    if any(v in writes and c != writes[v] for v, c in reads):
+        return None
+    return {"outer": outer, "ovars": ovars, "ivs": sorted(ivs), "reads": reads, "writes": writes}
 
 
 def _first_access_is_read(prog: Program, lid: int, vid: int) -> bool:
@@ -374,6 +447,13 @@ class _Gen:
                 if nst.shape == "flat" and nst.chain and all(
                         st.kind == "assign" for st in prog.regions[prog.loops[nst.chain[-1]].body].statements):
                     nst.ppt = int(spec["flat_ppt"])
+        if int(spec.get("flat_vec", QUAD)) == QUAD and not spec.get("flat_ppt") \
+                and int(spec.get("flat_kblock", 1)) == 1:
+            for nst in self.nests.values():
+                if nst.shape == "flat" and nst.chain:
+                    qp = quad_plan(prog, nst.chain, self.precision)
+                    if qp is not None:
+                        nst.shape, nst.quad, nst.ppt = "quad", qp, 1
         self.device_op = {}
         for l in prog.loops:
             self.device_op[l.id] = any(st.kind == "replaced" for st in prog.walk(l.body))
@@ -599,6 +679,12 @@ class _Gen:
             out.append("  }")
             D = len(n.chain)
             out.append(f"  for (int d = 0; d < {D}; ++d) a.tn[d] = a.n[d];")
+            if n.shape == "quad":
+                # quads per row: the row's first element may sit anywhere in
+                # its aligned chunk, so one extra (possibly empty) quad
+                out.append(f"  a.tn[{D - 1}] = (a.n[{D - 1}] + {QUAD - 1}) / {QUAD} + 1;")
+                out.append("  total = 1;")
+                out.append(f"  for (int d = 0; d < {D}; ++d) total *= a.tn[d];")
             if n.kb > 1:
                 out.append(f"  a.tn[{D - 1}] = (a.n[{D - 1}] + {n.kb - 1}) / {n.kb};")
                 out.append("  total = 1;")
@@ -661,6 +747,8 @@ class _Gen:
             return self.stencil_kernel_fn(n)
         if n.shape == "brick":
             return self.brick_kernel_fn(n)
+        if n.shape == "quad":
+            return self.quad_kernel_fn(n)
         prog = self.prog
         lid = n.root
         U = n.ppt
@@ -738,6 +826,114 @@ class _Gen:
             out.append("    }")
         else:
             out.append("    point(t0);")
+        out.append("  }")
+        out.append("}")
+        return out
+
+    def quad_kernel_fn(self, n: NestPlan) -> list[str]:
+        """Vectorised flat kernel (see :func:`quad_plan`): one thread per
+        16-byte-aligned quad of a row of the innermost loop.  Every array
+        reference becomes a lane of an aligned ``float4``/``int4`` chunk
+        loaded once per thread (the 19 ``p`` reads of the Himeno Jacobi body
+        share 18 chunks; the 12 coefficient arrays one chunk each), so the
+        LSU issues ~8x fewer load instructions than the scalar flat kernel.
+        Lanes outside the loop's range are masked at the store; aligned
+        writes of fully valid quads are single 16-byte stores.  Each lane
+        evaluates the same C expression tree as the CPU path (bit-exact)."""
+        prog = self.prog
+        lid = n.root
+        qp = n.quad
+        D = len(n.chain)
+        iv = [prog.loops[c].index_var for c in n.chain]
+        kv = iv[-1]
+        minb = self.spec.get("flat_min_blocks")
+        lb = f"{BLOCK_THREADS}, {int(minb)}" if minb else f"{BLOCK_THREADS}"
+        out = [f'extern "C" __global__ void __launch_bounds__({lb}) {n.kernel}(const KA_L{lid} a) {{']
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        out.extend(self._locals(n, "  "))
+        out.append("  const uint32_t stride = gridDim.x * blockDim.x;")
+        out.append("  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {")
+        out.append("    if (t == a.total - 1u) {")
+        out.extend(self._finals(n, "      "))
+        out.append("    }")
+        out.append("    uint32_t r = t;")
+        for d in range(D - 1, 0, -1):
+            nm = "q_" if d == D - 1 else f"v{iv[d]}_"
+            out.append(f"    uint32_t {nm};")
+            out.append(f"    {{ uint32_t q = b2o_fastdiv(r, a.mul[{d}], a.shr[{d}]); {nm} = r - q * a.tn[{d}]; r = q; }}")
+        if D == 1:
+            out.append("    const uint32_t q_ = r;")
+        else:
+            out.append(f"    const uint32_t v{iv[0]}_ = r;")
+        for d in range(D - 1):
+            out.append(f"    const int32_t v{iv[d]} = a.lo[{d}] + (int32_t)v{iv[d]}_;")
+        row = [f"(int64_t){c} * v{v}" for v, c in zip(qp["ovars"], qp["outer"]) if c]
+        out.append(f"    const int64_t F_ = {' + '.join(row) if row else '0'};")
+        out.append(f"    const int64_t b_ = ((F_ + a.lo[{D - 1}]) & ~(int64_t){QUAD - 1}) + (int64_t){QUAD} * q_;")
+        out.append(f"    const int32_t k0_ = (int32_t)(b_ - F_);")
+        out.append(f"    const int32_t kr_ = k0_ - a.lo[{D - 1}];")
+        out.append(f"    const int32_t kn_ = (int32_t)a.n[{D - 1}];")
+        out.append(f"    if (kr_ + {QUAD - 1} < 0 || kr_ >= kn_) continue;")
+        out.append(f"    const bool full_ = kr_ >= 0 && kr_ + {QUAD} <= kn_;")
+        # aligned chunks every read needs
+        chunks = sorted({(v, (c + u) // QUAD) for v, c in qp["reads"] for u in range(QUAD)})
+
+        def cname(v, o):
+            return f"c{v}_{'m' if o < 0 else ''}{abs(o)}"
+
+        for v, o in chunks:
+            vt = "float4" if self.T(v) == "float" else "int4"
+            ld = "__ldg" if v not in qp["writes"] else ""  # read-only path only for arrays the nest never writes
+            out.append(f"    const {vt} {cname(v, o)} = {ld}(reinterpret_cast<const {vt} *>(v{v} + b_)[{o}]);"
+                       if not ld else
+                       f"    const {vt} {cname(v, o)} = __ldg(reinterpret_cast<const {vt} *>(v{v} + b_) + ({o}));")
+        ivs = set(qp["ivs"])
+
+        latest: dict[int, int] = {}  # array -> statement whose lane values it now holds
+
+        def lane_expr(e, u):
+            k = e[0]
+            if k == "arr" and e[1] in latest:
+                return f"r{latest[e[1]]}_{u}"
+            if k == "arr":
+                c = affine(e[2], ivs)[1]
+                el = c + u
+                return f"{cname(e[1], el // QUAD)}.{'xyzw'[el % QUAD]}"
+            if k == "var" and e[1] == kv:
+                return f"(k0_ + {u})"
+            if k in ("num", "var"):
+                return render(e, self.local_name)
+            return f"({lane_expr(e[2], u)} {e[1]} {lane_expr(e[3], u)})"
+
+        body = prog.regions[prog.loops[n.chain[-1]].body].statements
+        for si, st in enumerate(body):
+            v = st.target[1]
+            T = self.T(v)
+            for u in range(QUAD):
+                out.append(f"    const {T} r{si}_{u} = ({T})({lane_expr(st.value, u)});")
+            latest[v] = si
+        for si, st in enumerate(body):
+            v = st.target[1]
+            c = qp["writes"][v]
+            lanes = [f"r{si}_{u}" for u in range(QUAD)]
+            masked = [f"      if ((uint32_t)(kr_ + {u}) < (uint32_t)kn_) v{v}[b_ + ({c + u})] = {lanes[u]};"
+                      for u in range(QUAD)]
+            if c % QUAD == 0:
+                vt = "float4" if self.T(v) == "float" else "int4"
+                mk = "make_float4" if vt == "float4" else "make_int4"
+                out.append("    if (full_) {")
+                out.append(f"      reinterpret_cast<{vt} *>(v{v} + b_)[{c // QUAD}] = {mk}({', '.join(lanes)});")
+                out.append("    } else {")
+                out.extend(masked)
+                out.append("    }")
+            else:
+                out.append("    {")
+                out.extend(masked)
+                out.append("    }")
+        for v in n.locals_:
+            out.append(f"    (void)v{v};")
         out.append("  }")
         out.append("}")
         return out
@@ -1103,7 +1299,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap")}
+                                     "flat_grid_cap", "flat_vec")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

@@ -44,6 +44,8 @@
 
 namespace {
 
+constexpr size_t kB2oGuard = 256;  // bytes of slack before and after each device array
+
 thread_local std::string g_err;
 std::mutex g_mu;
 
@@ -81,7 +83,11 @@ struct AppDev {
   Worker *w = nullptr;
   CUmodule mod = nullptr;
   std::vector<CUfunction> kfun;
-  std::vector<void *> host, dev, dev_pristine;
+  // dev[v] points kB2oGuard bytes into its allocation (dev_alloc[v]): the
+  // vectorised (quad) kernels load whole aligned 16-byte chunks, so a masked
+  // lane next to the first/last element may touch up to 12 bytes outside the
+  // array; the guard keeps those loads inside the allocation
+  std::vector<void *> host, dev, dev_alloc, dev_pristine;
   void *cells = nullptr;     // pinned 8-byte scalar cells
   void *slab = nullptr;      // device scalar slab
   void *slab_init = nullptr; // pinned initial slab contents
@@ -467,6 +473,7 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
   }
   d->host.assign(nv, nullptr);
   d->dev.assign(nv, nullptr);
+  d->dev_alloc.assign(nv, nullptr);
   d->dev_pristine.assign(nv, nullptr);
   if (cudaHostAlloc(&d->cells, 8 * (size_t)std::max(nv, 1), cudaHostAllocPortable) != cudaSuccess)
     return fail("pinned alloc of scalar cells");
@@ -485,7 +492,10 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
     }
     if (cudaHostAlloc(&d->host[v], bytes, cudaHostAllocPortable) != cudaSuccess)
       return fail("pinned alloc %zu B for %s", bytes, vi.name);
-    if (cudaMalloc(&d->dev[v], bytes) != cudaSuccess) return fail("device alloc %zu B for %s", bytes, vi.name);
+    if (cudaMalloc(&d->dev_alloc[v], bytes + 2 * kB2oGuard) != cudaSuccess)
+      return fail("device alloc %zu B for %s", bytes, vi.name);
+    cudaMemset(d->dev_alloc[v], 0, bytes + 2 * kB2oGuard);
+    d->dev[v] = (char *)d->dev_alloc[v] + kB2oGuard;
     if (cudaMemcpy(d->dev[v], a->initial[v].data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess)
       return fail("initial upload of %s", vi.name);
     if (vi.written) {
@@ -858,7 +868,7 @@ int b2o_shutdown(void) {
     for (auto &d : a->per_worker) {
       if (!d) continue;
       cudaSetDevice(d->w->device);
-      for (void *p : d->dev) if (p) cudaFree(p);
+      for (void *p : d->dev_alloc) if (p) cudaFree(p);
       for (void *p : d->dev_pristine) if (p) cudaFree(p);
       for (size_t v = 0; v < d->host.size(); ++v)
         if (a->info->vars[v].is_array && d->host[v]) cudaFreeHost(d->host[v]);
@@ -988,7 +998,7 @@ int b2o_app_destroy(uint64_t app) {
     if (!d) continue;
     cudaSetDevice(d->w->device);
     cudaStreamSynchronize(d->w->stream);
-    for (void *p : d->dev) if (p) cudaFree(p);
+    for (void *p : d->dev_alloc) if (p) cudaFree(p);
     for (void *p : d->dev_pristine) if (p) cudaFree(p);
     for (size_t v = 0; v < d->host.size(); ++v)
       if (a->info->vars[v].is_array && d->host[v]) cudaFreeHost(d->host[v]);
