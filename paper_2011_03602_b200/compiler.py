@@ -453,6 +453,7 @@ class _Gen:
                 if nst.shape == "flat" and nst.chain:
                     qp = quad_plan(prog, nst.chain, self.precision)
                     if qp is not None:
+                        qp["groups"] = int(spec.get("quad_groups", 1))
                         nst.shape, nst.quad, nst.ppt = "quad", qp, 1
         self.device_op = {}
         for l in prog.loops:
@@ -682,7 +683,8 @@ class _Gen:
             if n.shape == "quad":
                 # quads per row: the row's first element may sit anywhere in
                 # its aligned chunk, so one extra (possibly empty) quad
-                out.append(f"  a.tn[{D - 1}] = (a.n[{D - 1}] + {QUAD - 1}) / {QUAD} + 1;")
+                L = QUAD * n.quad["groups"]
+                out.append(f"  a.tn[{D - 1}] = (a.n[{D - 1}] + {QUAD - 1 + L - 1}) / {L};")
                 out.append("  total = 1;")
                 out.append(f"  for (int d = 0; d < {D}; ++d) total *= a.tn[d];")
             if n.kb > 1:
@@ -871,14 +873,15 @@ class _Gen:
             out.append(f"    const int32_t v{iv[d]} = a.lo[{d}] + (int32_t)v{iv[d]}_;")
         row = [f"(int64_t){c} * v{v}" for v, c in zip(qp["ovars"], qp["outer"]) if c]
         out.append(f"    const int64_t F_ = {' + '.join(row) if row else '0'};")
-        out.append(f"    const int64_t b_ = ((F_ + a.lo[{D - 1}]) & ~(int64_t){QUAD - 1}) + (int64_t){QUAD} * q_;")
+        G = qp["groups"]
+        L = QUAD * G  # lanes (points) per thread: G aligned quads of one row
+        out.append(f"    const int64_t b_ = ((F_ + a.lo[{D - 1}]) & ~(int64_t){QUAD - 1}) + (int64_t){L} * q_;")
         out.append(f"    const int32_t k0_ = (int32_t)(b_ - F_);")
         out.append(f"    const int32_t kr_ = k0_ - a.lo[{D - 1}];")
         out.append(f"    const int32_t kn_ = (int32_t)a.n[{D - 1}];")
-        out.append(f"    if (kr_ + {QUAD - 1} < 0 || kr_ >= kn_) continue;")
-        out.append(f"    const bool full_ = kr_ >= 0 && kr_ + {QUAD} <= kn_;")
+        out.append(f"    if (kr_ + {L - 1} < 0 || kr_ >= kn_) continue;")
         # aligned chunks every read needs
-        chunks = sorted({(v, (c + u) // QUAD) for v, c in qp["reads"] for u in range(QUAD)})
+        chunks = sorted({(v, (c + u) // QUAD) for v, c in qp["reads"] for u in range(L)})
 
         def cname(v, o):
             return f"c{v}_{'m' if o < 0 else ''}{abs(o)}"
@@ -911,27 +914,29 @@ class _Gen:
         for si, st in enumerate(body):
             v = st.target[1]
             T = self.T(v)
-            for u in range(QUAD):
+            for u in range(L):
                 out.append(f"    const {T} r{si}_{u} = ({T})({lane_expr(st.value, u)});")
             latest[v] = si
         for si, st in enumerate(body):
             v = st.target[1]
             c = qp["writes"][v]
-            lanes = [f"r{si}_{u}" for u in range(QUAD)]
-            masked = [f"      if ((uint32_t)(kr_ + {u}) < (uint32_t)kn_) v{v}[b_ + ({c + u})] = {lanes[u]};"
-                      for u in range(QUAD)]
-            if c % QUAD == 0:
-                vt = "float4" if self.T(v) == "float" else "int4"
-                mk = "make_float4" if vt == "float4" else "make_int4"
-                out.append("    if (full_) {")
-                out.append(f"      reinterpret_cast<{vt} *>(v{v} + b_)[{c // QUAD}] = {mk}({', '.join(lanes)});")
-                out.append("    } else {")
-                out.extend(masked)
-                out.append("    }")
-            else:
-                out.append("    {")
-                out.extend(masked)
-                out.append("    }")
+            for g in range(G):
+                us = range(QUAD * g, QUAD * g + QUAD)
+                lanes = [f"r{si}_{u}" for u in us]
+                masked = [f"      if ((uint32_t)(kr_ + {u}) < (uint32_t)kn_) v{v}[b_ + ({c + u})] = r{si}_{u};"
+                          for u in us]
+                if c % QUAD == 0:
+                    vt = "float4" if self.T(v) == "float" else "int4"
+                    mk = "make_float4" if vt == "float4" else "make_int4"
+                    out.append(f"    if (kr_ + {QUAD * g} >= 0 && kr_ + {QUAD * g + QUAD} <= kn_) {{")
+                    out.append(f"      reinterpret_cast<{vt} *>(v{v} + b_)[{c // QUAD + g}] = {mk}({', '.join(lanes)});")
+                    out.append("    } else {")
+                    out.extend(masked)
+                    out.append("    }")
+                else:
+                    out.append("    {")
+                    out.extend(masked)
+                    out.append("    }")
         for v in n.locals_:
             out.append(f"    (void)v{v};")
         out.append("  }")
@@ -1299,7 +1304,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

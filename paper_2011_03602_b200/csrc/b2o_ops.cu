@@ -1,16 +1,21 @@
 // b2o_ops.cu — CPU bindings of opaque library calls and the shared-memory
-// radix-2 FFT that replaces cufft_exec (reference fixtures/sample_db.json:6).
+// FFT that replaces cufft_exec (reference fixtures/sample_db.json:6).
 //
 // FFT design (HBM-bound): two passes over HBM.
-//   pass 1: one CTA per row, the 4096-point row staged in shared memory
-//           (32 KB), bit-reversed on load, log2(n) radix-2 stages, coalesced
-//           store;
-//   pass 2: one CTA per group of 4 adjacent columns (32-byte sector per row),
-//           4 x 4096 points in 128 KB of shared memory, same butterflies.
+//   n = 4096 (the config-3 size): 4096 = 16 x 16 x 16 four-step factorisation,
+//     rows: one CTA per row, first radix-16 pass straight from HBM into
+//           registers, last one straight back, two XOR-swizzled shared-memory
+//           exchanges in between;
+//     cols: in place, one 16-CTA thread-block cluster per 16 adjacent columns
+//           (128-byte row segments); the last radix-16 pass gathers across
+//           the cluster through distributed shared memory.
+//   n = 256: Stockham radix-16 in shared memory; other powers of two: radix-2.
 // Twiddles are computed in double on the host and kept in a device table.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <cstdio>
 #include <cstring>
@@ -22,6 +27,8 @@
 #include "../../include/b2o.h"
 #include "b2o_module.h"
 #include "b2o_ops.h"
+
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------------------
 // CPU bindings (the "original library" an unreplaced program calls)
@@ -289,6 +296,161 @@ __global__ void __launch_bounds__(512, 2) fft16_cols_kernel(float2 *__restrict__
   }
 }
 
+// ---- 4096-point path: 4096 = 16 x 16 x 16 as a four-step factorisation
+//   n = n2 + 16 (b + 16 a),  k = k1a + 16 k1b + 256 k2
+//   X[k] = sum_n2 W16^(n2 k2) W4096^(n2 k1) sum_b W16^(b k1b) W256^(b k1a) sum_a W16^(a k1a) x[n]
+// pass 1 (DFT over a) reads HBM straight into registers, pass 3 (DFT over
+// n2) stores straight to HBM, so a 4096-point FFT costs two shared-memory
+// exchanges (XOR-swizzled: conflict-free) instead of four.
+
+// rows: one CTA (256 threads, 32 KB smem) per 4096-point row
+__global__ void __launch_bounds__(256) fft4k_rows_kernel(const float2 *__restrict__ x, float2 *__restrict__ y,
+                                                          const float2 *__restrict__ tw) {
+  __shared__ float2 s[4096];
+  const int t = threadIdx.x;
+  const float2 *src = x + (size_t)blockIdx.x * 4096;
+  float2 v[16];
+  // pass 1: thread (n2 = t & 15, b = t >> 4) owns n = t + 256 a
+#pragma unroll
+  for (int a = 0; a < 16; ++a) v[a] = src[t + 256 * a];
+  dft16(v);
+  {
+    const int n2 = t & 15, b = t >> 4;
+    const float2 w1 = tw[16 * b];
+    float2 w = w1;
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+      v[k] = cmul(v[k], w);
+      w = cmul(w, w1);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s[n2 * 256 + k * 16 + (b ^ n2)] = v[k];
+  }
+  __syncthreads();
+  // pass 2: thread (n2 = t & 15, k1a = t >> 4), DFT over b
+  {
+    const int n2 = t & 15, k1a = t >> 4;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) v[b] = s[n2 * 256 + k1a * 16 + (b ^ n2)];
+    __syncthreads();
+    dft16(v);
+    const float2 step = tw[16 * n2];
+    float2 w = tw[n2 * k1a];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v[k] = cmul(v[k], w);
+      w = cmul(w, step);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s[(k1a + 16 * k) * 16 + (n2 ^ k1a)] = v[k];
+  }
+  __syncthreads();
+  // pass 3: thread k1 = t, DFT over n2, coalesced stores X[k1 + 256 k2]
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) v[n2] = s[t * 16 + (n2 ^ (t & 15))];
+  dft16(v);
+  float2 *dst = y + (size_t)blockIdx.x * 4096;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) dst[t + 256 * k] = v[k];
+}
+
+// columns, in place: a thread-block CLUSTER of kClusterFft CTAs owns 16
+// adjacent columns (128-byte row segments: full sectors, one HBM read and one
+// write of every element).  CTA rank c holds the 256-point sub-FFTs of the
+// rows n2 = c*NPC .. (c+1)*NPC-1 (mod 16) in its shared memory; the final DFT
+// over n2 gathers its 16 inputs from the peer CTAs through distributed
+// shared memory (ld.shared::cluster), so the 4096-point column FFT never
+// round-trips through HBM.
+constexpr int kClusterFft = 16;
+
+template <int NPC>
+__global__ void __launch_bounds__(256 * NPC) fft4k_cols_cluster_kernel(float2 *__restrict__ y,
+                                                                        const float2 *__restrict__ tw) {
+  extern __shared__ float2 s[];  // NPC x 4096
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int CL = 16 / NPC;
+  const int c = (int)cl.block_rank();
+  const int col0 = (int)(blockIdx.x / CL) * 16;
+  const int t = threadIdx.x & 255, sub = threadIdx.x >> 8;
+  const int n2 = c * NPC + sub;
+  float2 *sz = s + sub * 4096;
+  const int cc = t & 15;
+  float2 v[16];
+  {
+    const int b = t >> 4;
+#pragma unroll
+    for (int a = 0; a < 16; ++a) v[a] = y[(size_t)(n2 + 16 * (b + 16 * a)) * 4096 + col0 + cc];
+    dft16(v);
+    const float2 w1 = tw[16 * b];
+    float2 w = w1;
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+      v[k] = cmul(v[k], w);
+      w = cmul(w, w1);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sz[(b * 16 + k) * 16 + cc] = v[k];
+  }
+  __syncthreads();
+  {
+    const int k1a = t >> 4;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) v[b] = sz[(b * 16 + k1a) * 16 + cc];
+    __syncthreads();
+    dft16(v);
+    const float2 step = tw[16 * n2];
+    float2 w = tw[n2 * k1a];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v[k] = cmul(v[k], w);
+      w = cmul(w, step);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sz[(k1a + 16 * k) * 16 + cc] = v[k];
+  }
+  // every CTA's Y[k1][cc] is published to the cluster
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  {
+    const int k1 = c * 16 * NPC + (threadIdx.x >> 4);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const float2 *peer = cl.map_shared_rank(s, m / NPC) + (m % NPC) * 4096;
+      v[m] = peer[k1 * 16 + cc];
+    }
+    dft16(v);
+    // done reading peers (release: orders the remote loads before the
+    // arrive); the wait at the end keeps this CTA's shared memory alive until
+    // every peer has read it, overlapping the HBM stores
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 16; ++k) y[(size_t)(k1 + 256 * k) * 4096 + col0 + cc] = v[k];
+  }
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+template <int NPC>
+cudaError_t launch_cols_cluster(float2 *y, const float2 *tw, cudaStream_t s) {
+  constexpr int CL = 16 / NPC;
+  auto kern = fft4k_cols_cluster_kernel<NPC>;
+  const size_t smem = sizeof(float2) * 4096 * NPC;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((4096 / 16) * CL);
+  cfg.blockDim = dim3(256 * NPC);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, y, tw);
+}
+
 std::mutex tw_mu;
 std::map<std::pair<int, int64_t>, float2 *> tw_cache;  // (device, n) -> table
 
@@ -328,6 +490,28 @@ extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) 
       cudaFuncSetAttribute(fft16_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       cudaFuncSetAttribute(fft16_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr16[dev & 63] = true;
+    }
+    if (n == 4096 && !getenv("B2O_FFT_LEGACY")) {
+      fft4k_rows_kernel<<<4096, 256, 0, s>>>((const float2 *)x, (float2 *)y, tw);
+      // cluster of 16 CTAs (non-portable size) when the device takes it, else 8 x 2 sub-FFTs
+      static int npc[64] = {0};
+      if (npc[dev & 63] == 0 && getenv("B2O_FFT_NPC")) npc[dev & 63] = atoi(getenv("B2O_FFT_NPC"));
+      if (npc[dev & 63] == 0) {
+        cudaError_t e = launch_cols_cluster<1>((float2 *)y, tw, s);
+        if (e == cudaSuccess) {
+          npc[dev & 63] = 1;
+        } else {
+          cudaGetLastError();
+          npc[dev & 63] = 2;
+          // the 16-CTA cluster did not launch (nothing ran): use 8 CTAs x 2 sub-FFTs
+          if (launch_cols_cluster<2>((float2 *)y, tw, s) != cudaSuccess) return -1;
+        }
+      } else if (npc[dev & 63] == 1) {
+        if (launch_cols_cluster<1>((float2 *)y, tw, s) != cudaSuccess) return -1;
+      } else {
+        if (launch_cols_cluster<2>((float2 *)y, tw, s) != cudaSuccess) return -1;
+      }
+      return cudaGetLastError() == cudaSuccess ? 0 : -1;
     }
     if (n != 4096 && n != 256) return -1;
     fft16_rows_kernel<<<(unsigned)n, (unsigned)(n / 16), sizeof(float2) * n, s>>>((const float2 *)x, (float2 *)y,
