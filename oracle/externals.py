@@ -8,7 +8,10 @@ and the fixture ``fft`` body is a placeholder, ``fixtures/three_loops_fft.mini:1
   and rounded once to the element type;
 * ``fft2d``: y = forward, unnormalised 2-D DFT of x (``numpy.fft.fft2``
   convention), both interleaved complex ``[re, im]`` row-major ``n x n``,
-  computed in complex128.
+  computed in complex128;
+* ``histogram``: ``h[d[i]] += 1`` over every element of the int array ``d``
+  in order (the DB comparison snippet ``h[d[n]] = h[d[n]] + 1.0``,
+  fixtures/sample_db.json:23), values outside ``[0, len(h))`` skipped.
 
 Operand binding mirrors ``paper_2011_03602_b200.appspec`` but is restated here
 so the checker does not import the product.
@@ -20,7 +23,7 @@ import math
 
 import numpy as np
 
-BLOCK_KINDS = {"cublas_gemm": "gemm", "cufft_exec": "fft2d"}
+BLOCK_KINDS = {"cublas_gemm": "gemm", "cufft_exec": "fft2d", "cuda_histogram": "histogram"}
 
 
 def gemm(a: np.ndarray, b: np.ndarray, m: int, n: int, k: int, dtype) -> np.ndarray:
@@ -52,6 +55,13 @@ def _apply(kind: str, out: int, ins: list[int], state, spec_desc: dict) -> None:
     elif kind == "fft2d":
         n = int(spec_desc.get("n", math.isqrt(state[ins[0]].shape[0] // 2)))
         state[out][:] = fft2d(state[ins[0]], n, dtype)
+    elif kind == "histogram":
+        d = state[ins[0]].astype(np.int64)
+        bins = state[out].shape[0]
+        d = d[(d >= 0) & (d < bins)]
+        counts = np.bincount(d, minlength=bins)
+        state[out][:] = (state[out].astype(np.float64) + counts).astype(dtype) if dtype != np.int32 \
+            else (state[out] + counts.astype(np.int32))
     else:
         raise ValueError(f"unknown external kind {kind!r}")
 

@@ -12,8 +12,9 @@ loops do not, ``src/blocks.py:480-563``):
   ``rel_tol`` and a ``compare`` mode (``elementwise`` is the reference rule
   ``|c-r| <= max(rel*|r|, 1e-12)``, ``src/evaluators.py:129-139``;
   ``normwise`` is the documented deviation for FFT/GEMM outputs).
-* ``externals``: CPU semantics of opaque calls (``gemm``/``fft``), A.5.
-* ``blocks``: shapes of replaced function blocks (``cublas_gemm``/``cufft_exec``).
+* ``externals``: CPU semantics of opaque calls (``gemm``/``fft``/``histogram``), A.5.
+* ``blocks``: shapes of replaced function blocks (``cublas_gemm``/``cufft_exec``/
+  ``cuda_histogram``).
 """
 
 from __future__ import annotations
@@ -87,7 +88,8 @@ def outputs_of(prog: Program, spec: dict) -> list[tuple[int, float, str]]:
     return out
 
 
-EXTERNAL_KINDS = ("gemm", "fft2d")
+EXTERNAL_KINDS = ("gemm", "fft2d", "histogram")
+BLOCK_KINDS = {"cublas_gemm": "gemm", "cufft_exec": "fft2d", "cuda_histogram": "histogram"}
 
 
 def external_binding(spec: dict, name: str) -> dict | None:
@@ -108,7 +110,7 @@ def block_binding(prog: Program, spec: dict, stmt) -> dict:
     name = rb["name"]
     args = list(rb["args"])
     desc = dict(spec.get("blocks", {}).get(name, {}))
-    kind = desc.get("kind") or {"cublas_gemm": "gemm", "cufft_exec": "fft2d"}.get(name)
+    kind = desc.get("kind") or BLOCK_KINDS.get(name)
     if kind is None:
         raise ValueError(f"no block semantics for replacement {name!r}")
     set_vars = [v for v, k in stmt.occurrences if k == "set" and v in args]
@@ -136,7 +138,20 @@ def block_binding(prog: Program, spec: dict, stmt) -> dict:
         if 2 * n * n != lx or prog.vars[out].length != lx:
             raise ValueError(f"fft2d size {n} does not match operand lengths")
         binding.update(n=n)
+    elif kind == "histogram":
+        _histogram_shape(prog, binding)
     return binding
+
+
+def _histogram_shape(prog: Program, binding: dict) -> None:
+    """``cuda_histogram(d, h)`` (fixtures/sample_db.json:20-28, interface
+    ``int[], int[]``): ``h[d[i]] += 1`` for every element of ``d``; bins =
+    len(h).  Values outside [0, bins) are skipped (the original C loop would
+    write out of bounds)."""
+    d = binding["ins"][0]
+    if prog.vars[d].base_type != "int":
+        raise ValueError("histogram data must be an int array")
+    binding.update(m=prog.vars[binding["out"]].length, n=prog.vars[d].length)
 
 
 def external_call_binding(prog: Program, spec: dict, call) -> dict:
@@ -154,6 +169,8 @@ def external_call_binding(prog: Program, spec: dict, call) -> dict:
         binding.update(m=int(desc.get("m", n)), n=int(desc.get("n", n)), k=int(desc.get("k", n)))
     elif desc["kind"] == "fft2d":
         binding.update(n=int(desc.get("n", math.isqrt(prog.vars[ins[0]].length // 2))))
+    elif desc["kind"] == "histogram":
+        _histogram_shape(prog, binding)
     else:
         raise ValueError(f"unknown external kind {desc['kind']!r}")
     return binding

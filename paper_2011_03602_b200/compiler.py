@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-14"
+COMPILER_VERSION = "b2o-compiler-15"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 STENCIL_TILE = (32, 8)      # (k, j) tile of the 2.5-D stencil kernels
@@ -1265,7 +1265,7 @@ class _Gen:
         def op_row(b):
             if b is None:
                 return "  {-1, 0, 0, 0, 0, 0, 0},"
-            op = 0 if b["kind"] == "gemm" else 1
+            op = {"gemm": 0, "fft2d": 1, "histogram": 2}[b["kind"]]
             ins = b["ins"] + [-1, -1]
             return (f"  {{{op}, {b['out']}, {ins[0]}, {ins[1]}, {b.get('m', b.get('n', 0))}, "
                     f"{b.get('n', 0)}, {b.get('k', 0)}}},")

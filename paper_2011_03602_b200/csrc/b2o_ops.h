@@ -12,6 +12,8 @@ extern "C" {
 void b2o_cpu_gemm(const void *A, const void *B, void *C, int64_t m, int64_t n, int64_t k, int elem);
 // host: y = forward 2-D DFT of x (interleaved complex, n x n), double precision
 void b2o_cpu_fft2d(const void *x, void *y, int64_t n, int elem);
+// host: h[d[i]] += 1 for i < n (values outside [0, bins) skipped), h of b2o_elem elem
+void b2o_cpu_histogram(const int32_t *d, int64_t n, void *h, int64_t bins, int elem);
 
 #ifdef __cplusplus
 }

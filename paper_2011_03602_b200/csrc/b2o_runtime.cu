@@ -375,7 +375,8 @@ void cb_block(b2o_exec *ex, int32_t block) {
   d->mode = B2O_MODE_COHERENT;
   ensure_dev(d, op.in0, &d->acc.block_bytes);
   if (op.in1 >= 0) ensure_dev(d, op.in1, &d->acc.block_bytes);
-  d->dv[op.out] = 1;  // fully overwritten
+  if (op.op == B2O_OP_HISTOGRAM) ensure_dev(d, op.out, &d->acc.block_bytes);  // h += counts
+  d->dv[op.out] = 1;  // fully overwritten (gemm, fft) or updated on the device (histogram)
   d->mode = saved;
   if (ex->stop) return;
   int rc = 0;
@@ -386,6 +387,9 @@ void cb_block(b2o_exec *ex, int32_t block) {
     }
     rc = b2o_gemm_f32((const float *)d->dev[op.in0], (const float *)d->dev[op.in1], (float *)d->dev[op.out],
                       op.m, op.n, op.k, d->w->stream);
+  } else if (op.op == B2O_OP_HISTOGRAM) {
+    rc = b2o_histogram((const int32_t *)d->dev[op.in0], op.n, d->dev[op.out], op.m, VI(d, op.out).elem,
+                       d->w->stream);
   } else {
     if (d->app->info->precision != B2O_F32) {
       set_error(d, B2O_RUNTIME_ERROR, "cufft_exec replacement supports fp32 apps only");
@@ -418,6 +422,8 @@ void cb_external(b2o_exec *ex, int32_t call) {
   int elem = VI(d, op.out).elem;
   if (op.op == B2O_OP_GEMM) {
     b2o_cpu_gemm(d->host[op.in0], d->host[op.in1], d->host[op.out], op.m, op.n, op.k, elem);
+  } else if (op.op == B2O_OP_HISTOGRAM) {
+    b2o_cpu_histogram((const int32_t *)d->host[op.in0], op.n, d->host[op.out], op.m, elem);
   } else {
     b2o_cpu_fft2d(d->host[op.in0], d->host[op.out], op.n, elem);
   }

@@ -49,7 +49,7 @@ from gpuoffload.patterns import GenomeSpace, build_genome_space, pattern_from_ge
 from gpuoffload.screen import screen_model  # noqa: E402
 from gpuoffload.transfers import HOST_TO_DEVICE, TransferPlan, plan_transfers, unhoisted_plan  # noqa: E402
 
-from paper_2011_03602_b200.apps import blockapp, himeno, matmul, nasmg  # noqa: E402
+from paper_2011_03602_b200.apps import blockapp, histapp, himeno, matmul, nasmg  # noqa: E402
 
 
 def fixture(name: str) -> str:
@@ -190,6 +190,12 @@ def main() -> None:
     m = parse_mini_source(fixture("three_loops_fft.mini"))
     spec = uniform_spec(m, 11)  # x has 64 floats: no n with 2*n*n == 64, so the FFT variant cannot bind
     (HERE / "blocks_f2.json").write_text(json.dumps(block_record("blocks_f2", m, spec), sort_keys=True) + "\n")
+    # cuda_histogram (third DB record): name path (opaque call) + similarity path (loop)
+    for name, (n, bins) in {"blocks_hist": (4096, 64), "blocks_hist_16m": (1 << 24, 256)}.items():
+        m = parse_mini_source(histapp.source(n, bins))
+        rec = block_record(name, m, histapp.spec(n, bins))
+        rec["ga"] = app_record(name, m, histapp.spec(n, bins))
+        (HERE / f"{name}.json").write_text(json.dumps(rec, sort_keys=True) + "\n")
     print("wrote", sorted(p.name for p in HERE.glob("*.json")))
 
 

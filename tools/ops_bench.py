@@ -26,6 +26,7 @@ def timed(fn, iters=10, warm=3):
 
 
 L = lib()
+L.b2o_histogram.argtypes  # bound in runtime.lib()
 st = torch.cuda.current_stream().cuda_stream
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 a = torch.rand(n, n, device="cuda")
@@ -47,3 +48,10 @@ print(json.dumps({"op": "fft2d", "n": n, "ms": round(ms, 4), "gbs_two_pass": rou
 xc = torch.view_as_complex(x.view(n, n, 2))
 ms_cufft = timed(lambda: torch.fft.fft2(xc))
 print(json.dumps({"op": "cufft_c2c_2d", "ms": round(ms_cufft, 4)}))
+nh = 1 << 26  # 64M int32 = 256 MB > L2
+d = torch.randint(0, 256, (nh,), dtype=torch.int32, device="cuda")
+h = torch.zeros(256, dtype=torch.int32, device="cuda")
+ms = timed(lambda: L.b2o_histogram(d.data_ptr(), nh, h.data_ptr(), 256, 0, st))
+print(json.dumps({"op": "histogram", "n": nh, "bins": 256, "ms": round(ms, 4), "gbs": round(4 * nh / ms / 1e6, 1)}))
+ms_t = timed(lambda: torch.bincount(d, minlength=256))
+print(json.dumps({"op": "torch_bincount", "ms": round(ms_t, 4)}))
