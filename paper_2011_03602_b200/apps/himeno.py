@@ -98,9 +98,17 @@ def source(size: str | tuple[int, int, int] = "M", nn: int = 4, form: str = "inl
     return out
 
 
-def spec(size: str | tuple[int, int, int] = "M", form: str = "inline", precision: str = "fp32") -> dict:
+def spec(size: str | tuple[int, int, int] = "M", form: str = "inline", precision: str = "fp32",
+         reductions: bool = False) -> dict:
     """App spec: standard initmt inputs, outputs read by the final host
-    statement, fp32 tolerance 1e-5 (BASELINE.md parity tolerances)."""
+    statement, fp32 tolerance 1e-5 (BASELINE.md parity tolerances).
+
+    ``reductions=True`` is the opt-in of reductions.py (gosa reduced on the
+    GPU): the tree-ordered sum differs from the sequential fp32 sum by the
+    latter's rounding error -- at size M the sequential fp32 gosa is 2.5 %
+    above the exact (float64) sum of the same gs values, while the GPU tree
+    sum agrees with it to ~1e-7 (tests/test_reductions.py) -- so ``gosa`` and
+    ``chk`` are compared at 5e-2 (documented deviation; p and gs keep 1e-5)."""
     I, J, K = SIZES[size] if isinstance(size, str) else size
     inputs = {
         "p": {"kind": "himeno_p", "dims": [I, J, K]},
@@ -116,12 +124,18 @@ def spec(size: str | tuple[int, int, int] = "M", form: str = "inline", precision
     }
     outs = ["p", "gosa", "chk"] + (["gs"] if form == "inline" else [])
     rel = 1e-5 if precision == "fp32" else 1e-12
-    return {
+    out = {
         "name": f"himeno_{form}_{'x'.join(map(str, (I, J, K)))}",
         "precision": precision,
         "inputs": inputs,
         "outputs": {o: {"rel_tol": rel} for o in outs},
     }
+    if reductions:
+        out["reductions"] = True
+        out["name"] += "_red"
+        for o in ("gosa", "chk"):
+            out["outputs"][o]["rel_tol"] = 5e-2 if precision == "fp32" else 1e-9
+    return out
 
 
 def interior_points(size: str | tuple[int, int, int] = "M") -> int:

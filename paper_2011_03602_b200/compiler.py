@@ -36,13 +36,13 @@ import threading
 from dataclasses import dataclass
 from pathlib import Path
 
-from . import appspec
+from . import appspec, reductions
 from .ir import Program, expr_vars
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-15"
+COMPILER_VERSION = "b2o-compiler-16"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 STENCIL_TILE = (32, 8)      # (k, j) tile of the 2.5-D stencil kernels
@@ -101,15 +101,22 @@ def render(e, name) -> str:
 # ---------------------------------------------------------------------------
 
 
-def parallelizable(prog: Program, lid: int) -> bool:
+def parallelizable(prog: Program, lid: int, extended: bool = False) -> bool:
     """The reference's screen (src/screen.py:33-79), restated on the IR
     document: no non-index scalar both read and set in the subtree, every array
-    write indexed by this loop's index variable, no impure call."""
+    write indexed by this loop's index variable, no impure call.  With
+    ``extended`` (the opt-in of reductions.py) carried scalars that are
+    reductions or private temporaries are allowed."""
     loop = prog.loops[lid]
     if prog.doc["loops"][lid].get("directive_error", False):
         return False
     regions = set(prog.subtree_regions(lid))
     exempt = {prog.loops[x].index_var for x in prog.subtree_loops(lid)}
+    if extended:
+        cls = reductions.classify(prog, lid)
+        if cls is None:
+            return False
+        exempt |= set(cls)
     reads, sets = set(), set()
     for o in prog.doc["occurrences"]:
         if o["region"] not in regions or prog.vars[o["var"]].is_array or o["var"] in exempt:
@@ -149,6 +156,7 @@ class NestPlan:
     staged: dict = None     # stencil kernels: var -> {ci, cj, dmin, planes}
     streams: dict = None    # stencil kernels: var -> {ci, base}: one affine read per point
     quad: dict = None       # quad kernels: quad_plan() result
+    reds: dict = None       # reduction scalars of a chained nest: var -> "+" | "-" (reductions.py)
 
 
 def affine(e, idx_vars):
@@ -365,7 +373,7 @@ def _first_access_is_read(prog: Program, lid: int, vid: int) -> bool:
     return bool(loop_first(lid))
 
 
-def plan_nest(prog: Program, lid: int, enable_stencil: bool = False) -> NestPlan:
+def plan_nest(prog: Program, lid: int, enable_stencil: bool = False, extended: bool = False) -> NestPlan:
     loop = prog.loops[lid]
     nest_loops = prog.subtree_loops(lid)
     reads, writes = prog.subtree_access(lid)
@@ -389,7 +397,7 @@ def plan_nest(prog: Program, lid: int, enable_stencil: bool = False) -> NestPlan
         if st.kind in ("assign", "decl"):
             body_writes |= prog.stmt_access(st)[1]
     chain: list[int] = []
-    if parallelizable(prog, lid) and not (set(expr_vars(loop.lower)) | set(expr_vars(loop.upper))) & writes \
+    if parallelizable(prog, lid, extended) and not (set(expr_vars(loop.lower)) | set(expr_vars(loop.upper))) & writes \
             and loop.index_var not in body_writes:
         chain = [lid]
         while True:
@@ -400,7 +408,7 @@ def plan_nest(prog: Program, lid: int, enable_stencil: bool = False) -> NestPlan
             cl = prog.loops[c]
             bound_vars = set(expr_vars(cl.lower)) | set(expr_vars(cl.upper))
             chain_idx = {prog.loops[x].index_var for x in chain}
-            if (not parallelizable(prog, c) or bound_vars & (writes | chain_idx)
+            if (not parallelizable(prog, c, extended) or bound_vars & (writes | chain_idx)
                     or cl.index_var in chain_idx or cl.index_var in body_writes):
                 break
             chain.append(c)
@@ -417,9 +425,16 @@ def plan_nest(prog: Program, lid: int, enable_stencil: bool = False) -> NestPlan
     # roots evaluate chain bounds on the host: those reads are host-side
     need = set(scalar_args) | {a for a in arrays if a in reads} | bound_scalars
     swrites = sorted(set(chain_idx) | {v for v in locals_ if v in writes})
-    shape, ppt, staged, streams = _choose_shape(prog, chain, writes, enable_stencil)
+    reds = {}
+    if chain and extended:
+        cls = reductions.classify(prog, chain[0]) or {}
+        reds = {v: c.split(":")[1] for v, c in cls.items() if c.startswith("reduction")}
+        if len(reds) > 8:  # B2O_RED_MAX_VARS
+            chain, reds = [], {}
+    shape, ppt, staged, streams = _choose_shape(prog, chain, writes, enable_stencil and not reds)
     return NestPlan(lid, f"b2o_k{lid}", None, chain, sorted(need), sorted(writes), arrays,
-                    scalar_args, swrites, locals_, shape=shape, ppt=ppt, staged=staged, streams=streams)
+                    scalar_args, swrites, locals_, shape=shape, ppt=ppt, staged=staged, streams=streams,
+                    reds=reds or None)
 
 
 # ---------------------------------------------------------------------------
@@ -437,7 +452,8 @@ class _Gen:
         self.blocks: list[dict] = []
         self.block_ids: dict[int, int] = {}
         self.calls: dict[int, dict] = {}
-        self.nests = {l.id: plan_nest(prog, l.id, spec.get("stencil", False)) for l in prog.loops}
+        self.nests = {l.id: plan_nest(prog, l.id, spec.get("stencil", False), bool(spec.get("reductions")))
+                      for l in prog.loops}
         for nst in self.nests.values():
             if nst.shape == "flat" and nst.chain and nst.ppt == 1 and all(
                     st.kind == "assign" for st in prog.regions[prog.loops[nst.chain[-1]].body].statements):
@@ -652,7 +668,8 @@ class _Gen:
     def kernel_struct(self, n: NestPlan) -> list[str]:
         D = max(len(n.chain), 1)
         out = [f"typedef struct {{", "  uint32_t total, chunk;",
-               f"  uint32_t n[{D}], tn[{D}], mul[{D}], shr[{D}];", f"  int32_t lo[{D}];", "  void *slab;"]
+               f"  uint32_t n[{D}], tn[{D}], mul[{D}], shr[{D}];", f"  int32_t lo[{D}];", "  void *slab;",
+               "  void *scratch;"]
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
             out.append(f"  {const}{self.T(v)} *p{v};")
@@ -694,7 +711,7 @@ class _Gen:
             out.append("  if (total > 0xFFFFFFFFull) { ex->launch(ex, %d, 0, 0, 0); return; }" % lid)
             for d in range(1, len(n.chain)):
                 out.append(f"  b2o_fastdiv_init(a.tn[{d}], &a.mul[{d}], &a.shr[{d}]);")
-        out.append("  a.total = (uint32_t)total; a.slab = ex->slab;")
+        out.append("  a.total = (uint32_t)total; a.slab = ex->slab; a.scratch = ex->scratch;")
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
             out.append(f"  a.p{v} = ({const}{self.T(v)} *)ex->dev[{v}];")
@@ -717,6 +734,8 @@ class _Gen:
         else:
             per = BLOCK_THREADS * n.ppt
             cap = int(self.spec.get("flat_grid_cap", 0)) or 0x7FFFFFFF
+            if n.reds:
+                cap = min(cap, 2048)  # B2O_RED_MAX_BLOCKS: one partial per CTA in the scratch
             out.append(f"  {{ uint64_t g = (total + {per - 1}) / {per}; geom[0] = (uint32_t)(g > {cap}u ? "
                        f"{cap}u : g); geom[1] = geom[2] = 1; geom[3] = {BLOCK_THREADS}; geom[4] = geom[5] = 1; }}")
         out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, geom);")
@@ -728,6 +747,8 @@ class _Gen:
         chain_idx = [prog.loops[c].index_var for c in n.chain]
         out = []
         for v in n.swrites:
+            if n.reds and v in n.reds:
+                continue  # written by the reduction epilogue
             if v in chain_idx:
                 d = chain_idx.index(v)
                 val = f"a.lo[{d}] + (int32_t)a.n[{d}]"
@@ -760,6 +781,9 @@ class _Gen:
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
             out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        for v in (n.reds or {}):
+            out.append(f"  {self.T(v)} rd{v} = ({self.T(v)})0;  // per-thread partial of reduction {prog.vars[v].name}")
+        self._reds = n.reds or {}
         out.append("  auto point = [&](const uint32_t t) {")
         D = len(n.chain)
         for c in n.chain:
@@ -829,7 +853,38 @@ class _Gen:
         else:
             out.append("    point(t0);")
         out.append("  }")
+        self._reds = {}
+        if n.reds:
+            out.extend(self._reduction_epilogue(n))
         out.append("}")
+        return out
+
+    def _reduction_epilogue(self, n: NestPlan) -> list[str]:
+        """Deterministic grid reduction: block totals (warp xor-butterfly +
+        shared memory, b2o_block_sum) go to the scratch, one slot per CTA; the
+        last CTA to finish (atomic ticket) sums the slots in CTA order, adds
+        the value the scalar had at launch and stores it in the slab.  Fixed
+        grid => bit-reproducible run to run."""
+        out = ["  {", "    __shared__ double b2o_red_sm[32];", "    __shared__ int b2o_last;",
+               "    char *scr_ = (char *)a.scratch;", "    unsigned *cnt_ = (unsigned *)scr_;"]
+        for r, v in enumerate(n.reds):
+            T = self.T(v)
+            out.append(f"    {{ {T} bt = b2o_block_sum<{T}>(rd{v}, ({T} *)b2o_red_sm);")
+            out.append(f"      if (threadIdx.x == 0) (({T} *)(scr_ + 256 + {r} * 8 * B2O_RED_MAX_BLOCKS))[blockIdx.x] = bt; }}")
+        out.append("    if (threadIdx.x == 0) { __threadfence(); b2o_last = atomicAdd(cnt_, 1u) == gridDim.x - 1u; }")
+        out.append("    __syncthreads();")
+        out.append("    if (b2o_last) {")
+        out.append("      __threadfence();")
+        for r, v in enumerate(n.reds):
+            T = self.T(v)
+            out.append(f"      {{ const {T} *part = (const {T} *)(scr_ + 256 + {r} * 8 * B2O_RED_MAX_BLOCKS);")
+            out.append(f"        {T} s = ({T})0;")
+            out.append("        for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s = s + __ldcg(part + b);")
+            out.append(f"        s = b2o_block_sum<{T}>(s, ({T} *)b2o_red_sm);")
+            out.append(f"        if (threadIdx.x == 0) *({T} *)((char *)a.slab + 8 * {v}) = ({T})(a.s{v} + s); }}")
+        out.append("      if (threadIdx.x == 0) *cnt_ = 0u;")
+        out.append("    }")
+        out.append("  }")
         return out
 
     def quad_kernel_fn(self, n: NestPlan) -> list[str]:
@@ -1159,7 +1214,12 @@ class _Gen:
                 if st.init is not None:
                     out.append(pad + f"v{st.var} = {render(st.init, self.local_name)};")
             elif st.kind == "assign":
-                out.append(pad + f"{self.dev_expr(st.target)} = {self.dev_expr(st.value)};")
+                red = reductions.reduction_stmt(st) if getattr(self, "_reds", None) else None
+                if red is not None and red[0] in self._reds:
+                    v, op, e = red
+                    out.append(pad + f"rd{v} = rd{v} {op} ({self.dev_expr(e)});")
+                else:
+                    out.append(pad + f"{self.dev_expr(st.target)} = {self.dev_expr(st.value)};")
             elif st.kind == "loop":
                 self.dev_loop(st.loop, ind, out)
             elif st.kind == "call":
@@ -1304,7 +1364,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

@@ -91,6 +91,7 @@ struct AppDev {
   void *cells = nullptr;     // pinned 8-byte scalar cells
   void *slab = nullptr;      // device scalar slab
   void *slab_init = nullptr; // pinned initial slab contents
+  void *scratch = nullptr;   // device scratch for reduction partials (zeroed)
   std::vector<uint8_t> hv, dv, hmod, dev_dirty, host_touched;
   std::vector<uint8_t> is_root, dev_inside, hook_mask;
   std::vector<std::vector<b2o_directive>> hooks[2];
@@ -488,6 +489,8 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
   memset(d->cells, 0, 8 * (size_t)std::max(nv, 1));
   memset(d->slab_init, 0, 8 * (size_t)std::max(nv, 1));
   if (cudaMalloc(&d->slab, 8 * (size_t)std::max(nv, 1)) != cudaSuccess) return fail("device slab alloc");
+  if (cudaMalloc(&d->scratch, B2O_SCRATCH_BYTES) != cudaSuccess) return fail("device scratch alloc");
+  cudaMemset(d->scratch, 0, B2O_SCRATCH_BYTES);
   for (int v = 0; v < nv; ++v) {
     const b2o_var_info &vi = info->vars[v];
     size_t bytes = a->initial[v].size();
@@ -526,6 +529,7 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
   ex.host = d->host.data();
   ex.dev = d->dev.data();
   ex.slab = d->slab;
+  ex.scratch = d->scratch;
   ex.is_root = d->is_root.data();
   ex.dev_inside = d->dev_inside.data();
   ex.hook_mask = d->hook_mask.data();
@@ -881,6 +885,7 @@ int b2o_shutdown(void) {
       if (d->cells) cudaFreeHost(d->cells);
       if (d->slab_init) cudaFreeHost(d->slab_init);
       if (d->slab) cudaFree(d->slab);
+      if (d->scratch) cudaFree(d->scratch);
       if (d->mod) drv.moduleUnload(d->mod);
     }
   }
@@ -1011,6 +1016,7 @@ int b2o_app_destroy(uint64_t app) {
     if (d->cells) cudaFreeHost(d->cells);
     if (d->slab_init) cudaFreeHost(d->slab_init);
     if (d->slab) cudaFree(d->slab);
+    if (d->scratch) cudaFree(d->scratch);
     if (d->mod) drv.moduleUnload(d->mod);
   }
   if (a->dl) dlclose(a->dl);

@@ -49,7 +49,8 @@ from gpuoffload.patterns import GenomeSpace, build_genome_space, pattern_from_ge
 from gpuoffload.screen import screen_model  # noqa: E402
 from gpuoffload.transfers import HOST_TO_DEVICE, TransferPlan, plan_transfers, unhoisted_plan  # noqa: E402
 
-from paper_2011_03602_b200.apps import blockapp, histapp, himeno, matmul, nasmg  # noqa: E402
+from paper_2011_03602_b200.apps import blockapp, histapp, himeno, intsum, matmul, nasmg  # noqa: E402
+from paper_2011_03602_b200.reductions import screen_model_with_reductions  # noqa: E402
 
 
 def fixture(name: str) -> str:
@@ -93,13 +94,13 @@ def plan_record(model, pattern, plan) -> dict:
 
 
 def app_record(name: str, model, spec: dict, language: str | None = None, all_genomes_cap: int = 64,
-               extra_genomes=(), unhoisted=()) -> dict:
+               extra_genomes=(), unhoisted=(), screen=screen_model) -> dict:
     doc = model_to_document(model)
     if language:
         doc["language"] = language
         model = load_ir_document(json.dumps(doc))  # the reference validates the tagged document
         doc = model_to_document(model)
-    verdicts = screen_model(model)
+    verdicts = screen(model)
     space = build_genome_space(model, verdicts)
     genomes = list(space.all_genomes()) if 2 ** space.length <= all_genomes_cap else []
     for g in extra_genomes:
@@ -195,6 +196,22 @@ def main() -> None:
         m = parse_mini_source(histapp.source(n, bins))
         rec = block_record(name, m, histapp.spec(n, bins))
         rec["ga"] = app_record(name, m, histapp.spec(n, bins))
+        (HERE / f"{name}.json").write_text(json.dumps(rec, sort_keys=True) + "\n")
+    # opt-in reduction screen (reductions.py): the reference
+    # planner and genome encoder run on the extended verdicts
+    red = {
+        "himeno_xs_red": (parse_mini_source(himeno.source("XS", nn=3)), himeno.spec("XS", reductions=True),
+                          ("100100100", "000100000", "111111111", "001001001", "010010010", "000000000",
+                           "100000100", "000100100")),
+        "himeno_xs_temps_red": (parse_mini_source(himeno.source("XS", nn=3, form="temps")),
+                                himeno.spec("XS", form="temps", reductions=True), ()),
+        "himeno_M_red": (parse_mini_source(himeno.source("M", nn=20)), himeno.spec("M", reductions=True),
+                         ("100100100", "100000100", "000000000")),
+        "intsum": (parse_mini_source(intsum.source(1 << 16)), intsum.spec(1 << 16), ()),
+    }
+    for name, (m, spec, extra) in red.items():
+        rec = app_record(name, m, spec, extra_genomes=extra, screen=screen_model_with_reductions,
+                         all_genomes_cap=64 if not extra else 1)
         (HERE / f"{name}.json").write_text(json.dumps(rec, sort_keys=True) + "\n")
     print("wrote", sorted(p.name for p in HERE.glob("*.json")))
 
