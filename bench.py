@@ -263,6 +263,7 @@ def b200_arm(args, dist: Dist) -> None:
             r = ev.measure_payloads(g["doc"], [pat])[0]
             e2e.append((time.perf_counter() - t0, r))
         dist.barrier()
+    red = reductions_arm(args, dist) if args.reductions else None
     ga = ga_arm(args, dist) if args.ga else None
     ops = ops_arm(dist) if args.ops else None
     ms = dist.max(rep["ms_per_step"])
@@ -303,9 +304,35 @@ def b200_arm(args, dist: Dist) -> None:
         "app_speedup_vs_cpu": round(cpu_s / e2e_s, 2) if cpu_s else None,
         "ga": ga,
         "ops": ops,
+        "reductions_opt_in": red,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
+
+
+def reductions_arm(args, dist: Dist) -> dict:
+    """Opt-in reduction screen (reductions.py): the same Himeno M app with
+    the gosa nest offloaded too (genome 100100100: no per-sweep gs download,
+    no host gosa nest).  Not the headline (the genome differs from the
+    reference screen's); reported beside it, same bytes metric."""
+    from paper_2011_03602_b200.evaluator import B200Evaluator
+
+    g = golden("himeno_M_red")
+    nn = sweeps_of(g["doc"])
+    bytes_per_step = BYTES_PER_POINT * interior(SIZE) * nn
+    ev = B200Evaluator(g["spec"], devices=[dist.local_rank])
+    pat = g["patterns"]["100100100"]
+    ev.measure_payloads(g["doc"], [pat])
+    times, last = [], None
+    for _ in range(max(3, args.e2e_steps)):
+        t0 = time.perf_counter()
+        last = ev.measure_payloads(g["doc"], [pat])[0]
+        times.append(time.perf_counter() - t0)
+    e2e_s = dist.max(statistics.median(times))
+    return {"genome": "100100100", "validity": last["validity"], "e2e_GBps": round(bytes_per_step / e2e_s / 1e9, 3),
+            "ms_per_call": round(e2e_s * 1e3, 3), "app_run_ms": round(last["time_s"] * 1e3, 3),
+            "h2d_bytes": int(last["h2d_bytes"]), "d2h_bytes": int(last["d2h_bytes"]),
+            "note": "gosa tolerance 5e-2: the sequential fp32 reference sum is 2.5% off the exact sum"}
 
 
 def ga_arm(args, dist: Dist) -> dict | None:
@@ -331,14 +358,18 @@ def ga_arm(args, dist: Dist) -> dict | None:
     params = GAParams(population_size=args.ga_pop, generations=args.ga_gens, seed=args.ga_seed)
     dist.barrier()
     t0 = time.perf_counter()
-    res = run_search_batched(model, screen_model(model), evaluator, params)
+    stats: dict = {}
+    res = run_search_batched(model, screen_model(model), evaluator, params, stats=stats)
     wall = dist.max(time.perf_counter() - t0)
     valid = sum(1 for r in ev.log if r.get("validity") == "valid")
     local = dist.sum(float(len(ev.log)))
+    fit_sum = dist.sum(float(sum(r.get("time_s") or 0.0 for r in ev.log)))
     return {"workload": f"{args.ga_workload} inline nn={sweeps_of(g['doc'])}, pop {args.ga_pop} x {args.ga_gens} gens",
             "patterns_per_s": round(res.evaluations_performed / wall, 3), "evaluations": res.evaluations_performed,
             "cache_hits": res.cache_hits, "wall_s": round(wall, 3), "best_genome": "".join(map(str, res.best_genome)),
             "best_time_s": res.best_time, "measured_by_all_ranks": int(local), "valid_on_rank0": valid,
+            "speculated": stats.get("speculated", 0), "speculated_unused": stats.get("speculated_unused", 0),
+            "sum_fitness_s_all_ranks": round(fit_sum, 3),
             "history_evals": [h.evaluations for h in res.history][:6]}
 
 
@@ -382,6 +413,10 @@ def ops_arm(dist: Dist) -> dict:
     err = float(np.linalg.norm(c[:256].double().cpu().numpy() - (a[:256].double() @ b.double()).cpu().numpy())
                 / np.linalg.norm((a[:256].double() @ b.double()).cpu().numpy()))
     fft_ms = timed(lambda: L.b2o_fft2d_c64(x.data_ptr(), y.data_ptr(), n, st))
+    nh = 1 << 26  # 256 MB of int32 (> L2)
+    hd = torch.randint(0, 256, (nh,), dtype=torch.int32, device=dev)
+    hh = torch.zeros(256, dtype=torch.int32, device=dev)
+    hist_ms = timed(lambda: L.b2o_histogram(hd.data_ptr(), nh, hh.data_ptr(), 256, 0, st))
     pk = peaks()
     tf32_peak = pk["bf16_tflops"] / 2  # dense TF32 = half the dense BF16 rate on the same tensor pipe
     tf32_issued = 3 * 2 * n ** 3 / (gemm_ms * 1e-3) / 1e12
@@ -395,7 +430,12 @@ def ops_arm(dist: Dist) -> dict:
             "gemm_normwise_err_rows0_255": err,
             "fft_4096_ms": round(fft_ms, 4),
             "fft_roofline": {"bound": "hbm", "achieved": round(fft_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                             "frac": round(fft_gbs / pk["hbm_gbs"], 3), "bytes": "2 passes x read+write complex64"}}
+                             "frac": round(fft_gbs / pk["hbm_gbs"], 3), "bytes": "2 passes x read+write complex64"},
+            "histogram_64M_256bins_ms": round(hist_ms, 4),
+            "histogram_roofline": {"bound": "hbm", "achieved": round(4 * nh / (hist_ms * 1e-3) / 1e9, 1),
+                                   "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                   "frac": round(4 * nh / (hist_ms * 1e-3) / 1e9 / pk["hbm_gbs"], 3),
+                                   "bytes": "4 B read per element"}}
 
 
 def main() -> None:
@@ -406,7 +446,8 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--ga", type=int, default=1, help="also measure GA patterns/sec (config 5)")
-    ap.add_argument("--ops", type=int, default=1, help="also time the GEMM/FFT block kernels (config 3)")
+    ap.add_argument("--ops", type=int, default=1, help="also time the GEMM/FFT/histogram block kernels (config 3)")
+    ap.add_argument("--reductions", type=int, default=1, help="also time the opt-in reduction pattern")
     ap.add_argument("--ga-workload", default="himeno_L")
     ap.add_argument("--ga-pop", type=int, default=64)
     ap.add_argument("--ga-gens", type=int, default=20)

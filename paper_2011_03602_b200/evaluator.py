@@ -121,6 +121,12 @@ class B200Evaluator:
         self._docs: dict[int, tuple[object, dict]] = {}
         self.log: list[dict] = []
 
+    @property
+    def parallel_width(self) -> int:
+        """Patterns measured concurrently (one per B200 worker): the batch
+        drivers pad generations to a multiple of this (search.py)."""
+        return max(1, int(self.runtime.n_workers))
+
     # -- program management -------------------------------------------------
 
     def _doc(self, model) -> dict:

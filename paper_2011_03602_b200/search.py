@@ -10,6 +10,18 @@ deterministic evaluator the ``SearchResult`` is identical to ``run_search``'s
 (tests/test_search.py).  SPEC.md:286 allows exactly this ("results are merged
 in genome order so outcomes are independent of completion order").
 
+**Speculative prefetch, commit on demand** (SURVEY.md §8e).  When the
+evaluator measures ``parallel_width`` patterns at once (B200 workers x ranks)
+and a generation's fresh genomes do not fill the last round, the idle slots
+measure not-yet-requested genomes of the (small) genome space into a side
+cache.  A side-cache result is committed -- counted in
+``evaluations_performed``, reported to ``on_evaluation``, entered in the memo
+-- only when the GA later asks for that genome, so the ``SearchResult`` is
+still the reference's under a deterministic evaluator.  On Himeno L
+(64-genome space, fresh genomes per generation 62, 0, 0, 0, 0, 1, 1, ...)
+eight B200s then finish the whole search in the first round instead of
+paying two more serial rounds later.
+
 ``ShardedEvaluator`` spreads a batch over the ranks of a ``torch.distributed``
 process group (gloo, host-side results only: fitness units are independent,
 so there is no data-path collective): requests are assigned longest-predicted
@@ -32,7 +44,7 @@ def _ga():
 class _BatchRunner:
     """GenomeEvaluator (src/ga.py:85-134) with batch submission."""
 
-    def __init__(self, model, space, evaluator, backend, on_evaluation):
+    def __init__(self, model, space, evaluator, backend, on_evaluation, speculate: bool | None = None):
         ga = _ga()
         from gpuoffload.evaluators import EvaluationRequest
         from gpuoffload.model import ModelIndex, ReplacedBlock
@@ -50,6 +62,12 @@ class _BatchRunner:
         self.cache_hits = 0
         self.replaced_blocks = tuple(st for _, _, st in model.walk_statements() if isinstance(st, ReplacedBlock))
         self._needs_code = getattr(evaluator, "needs_code", True)
+        self.width = max(1, int(getattr(evaluator, "parallel_width", 1)))
+        if speculate is None:
+            speculate = self.width > 1 and space.length <= SPECULATE_MAX_BITS
+        self.speculate = speculate
+        self.side: dict = {}       # speculative (request, result) by genome, not yet committed
+        self.speculated = 0        # patterns measured speculatively
 
     def _request(self, bits, tags):
         from gpuoffload.codegen import emit_annotated
@@ -75,7 +93,19 @@ class _BatchRunner:
             if bits not in self.cache and bits not in seen:
                 seen.add(bits)
                 fresh.append(bits)
-        requests = [self._request(b, tags) for b in fresh]
+        fresh_res = {b: self.side.pop(b) for b in fresh if b in self.side}
+        to_measure = [b for b in fresh if b not in fresh_res]
+        extra: list[tuple] = []
+        if self.speculate and to_measure and len(to_measure) % self.width:
+            need = self.width - len(to_measure) % self.width
+            known = set(self.cache) | set(self.side) | set(fresh)
+            for g in self.space.all_genomes():
+                if len(extra) == need:
+                    break
+                if tuple(g) not in known:
+                    extra.append(tuple(g))
+        batch = to_measure + extra
+        requests = [self._request(b, tags) for b in batch]
         if requests:
             measure_batch = getattr(self.evaluator, "measure_batch", None)
             if measure_batch is not None:
@@ -84,9 +114,12 @@ class _BatchRunner:
                 results = [self.evaluator.measure(r) for r in requests]
         else:
             results = []
-        fresh_res = {}
-        for bits, req, res in zip(fresh, requests, results):
-            fresh_res[bits] = (req, res)
+        for bits, req, res in zip(batch, requests, results):
+            if bits in seen:
+                fresh_res[bits] = (req, res)
+            else:
+                self.side[bits] = (req, res)
+                self.speculated += 1
         out = []
         for bits in population:
             bits = tuple(bits)
@@ -104,15 +137,22 @@ class _BatchRunner:
         return out
 
 
-def run_search_batched(model, verdicts, evaluator, params, backend: str = "c_openacc", on_evaluation=None):
-    """``run_search`` (src/ga.py:246-285) with per-generation batch measurement."""
+SPECULATE_MAX_BITS = 12  # speculate only in genome spaces of <= 4096 patterns
+
+
+def run_search_batched(model, verdicts, evaluator, params, backend: str = "c_openacc", on_evaluation=None,
+                       speculate: bool | None = None, stats: dict | None = None):
+    """``run_search`` (src/ga.py:246-285) with per-generation batch
+    measurement (and speculative prefetch when ``speculate``; default: on
+    when the evaluator is wider than one pattern).  ``stats`` (optional dict)
+    receives ``speculated`` / ``speculated_unused`` counts."""
     ga = _ga()
     from gpuoffload.patterns import PatternError, build_genome_space
 
     space = build_genome_space(model, verdicts)
     if space.is_empty:
         raise PatternError("no offloadable loops; skip the search and use the CPU-only pattern")
-    runner = _BatchRunner(model, space, evaluator, backend, on_evaluation)
+    runner = _BatchRunner(model, space, evaluator, backend, on_evaluation, speculate)
     import random
 
     if space.length <= 2:
@@ -128,6 +168,8 @@ def run_search_batched(model, verdicts, evaluator, params, backend: str = "c_ope
             if gen + 1 < params.generations:
                 population = ga.next_generation(population, fits, params, rng)
         history = tuple(hist)
+    if stats is not None:
+        stats.update(speculated=runner.speculated, speculated_unused=len(runner.side))
     best_bits, best_time, no_offload = ga._best_of_cache(runner.cache, space.length)
     return ga.SearchResult(best_genome=best_bits, best_time=best_time, no_offload=no_offload,
                            evaluations_performed=runner.evaluations, cache_hits=runner.cache_hits,
@@ -192,6 +234,7 @@ class ShardedEvaluator:
         self.evaluator_id = getattr(inner, "evaluator_id", "sharded")
         self.concurrency_safe = True
         self.needs_code = getattr(inner, "needs_code", True)
+        self.parallel_width = self.world * max(1, int(getattr(inner, "parallel_width", 1)))
 
     def measure(self, request):
         return self.measure_batch([request])[0]

@@ -31,10 +31,13 @@ def sharded_ga(rank: int, world: int, port: int, seed: int, out_dir: str) -> Non
     model = random_model(random.Random(seed), max_depth=3)
     inner = Counting()
     ev = ShardedEvaluator(inner)
-    res = run_search_batched(model, screen_model(model), ev, GAParams(population_size=10, generations=6, seed=seed))
+    stats = {}
+    res = run_search_batched(model, screen_model(model), ev, GAParams(population_size=10, generations=6, seed=seed),
+                             stats=stats)
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump({"best": list(res.best_genome), "time": res.best_time, "evals": res.evaluations_performed,
                    "hits": res.cache_hits, "local_calls": inner.calls,
+                   "speculated_unused": stats["speculated_unused"],
                    "history": [[h.generation, h.best_time, h.mean_time, h.evaluations] for h in res.history]}, f)
     dist.barrier()
     dist.destroy_process_group()

@@ -55,6 +55,60 @@ def test_batched_ga_equals_reference(seed):
     assert sum(ev.batches) == b.evaluations_performed
 
 
+class WideCost(BatchCost):
+    """A BatchCost that claims to measure `width` patterns at once."""
+
+    def __init__(self, width):
+        super().__init__()
+        self.parallel_width = width
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_speculative_prefetch_commits_on_demand(seed):
+    """With idle slots filled by speculative genomes, the SearchResult and the
+    on_evaluation log are still the reference's (commit on demand), every
+    batch is a multiple of the width unless the space ran out, and
+    speculation never measures a genome twice."""
+    from gpuoffload.evaluators import CostModelEvaluator
+    from gpuoffload.ga import GAParams, run_search
+    from gpuoffload.screen import screen_model
+
+    from _models import random_model
+    from paper_2011_03602_b200.search import run_search_batched
+
+    model = random_model(random.Random(seed), max_depth=3)
+    params = GAParams(population_size=12, generations=8, seed=seed)
+    log_a, log_b = [], []
+    a = run_search(model, screen_model(model), CostModelEvaluator(), params,
+                   on_evaluation=lambda bits, req, res: log_a.append((bits, res.time_seconds)))
+    ev = WideCost(8)
+    stats = {}
+    b = run_search_batched(model, screen_model(model), ev, params, stats=stats,
+                           on_evaluation=lambda bits, req, res: log_b.append((bits, res.time_seconds)))
+    assert a == b
+    assert log_a == log_b
+    assert sum(ev.batches) == b.evaluations_performed + stats["speculated_unused"]
+    space = 2 ** b.genome_length
+    assert sum(ev.batches) <= space
+    for n in ev.batches[:-1]:
+        assert n % 8 == 0 or sum(ev.batches) == space
+
+
+def test_speculation_off_at_width_one():
+    from gpuoffload.ga import GAParams
+    from gpuoffload.screen import screen_model
+
+    from _models import random_model
+    from paper_2011_03602_b200.search import run_search_batched
+
+    model = random_model(random.Random(3), max_depth=3)
+    ev = BatchCost()
+    stats = {}
+    b = run_search_batched(model, screen_model(model), ev, GAParams(population_size=12, generations=8, seed=3),
+                           stats=stats)
+    assert stats["speculated"] == 0 and sum(ev.batches) == b.evaluations_performed
+
+
 def test_batched_exhaustive_equals_reference():
     from gpuoffload.evaluators import CostModelEvaluator
     from gpuoffload.ga import exhaustive_search
@@ -115,6 +169,8 @@ def test_sharded_ga_over_gloo_world2(tmp_path):
     for r in (r0, r1):
         assert tuple(r["best"]) == ref.best_genome and r["time"] == ref.best_time
         assert r["evals"] == ref.evaluations_performed and r["hits"] == ref.cache_hits
-    # each rank measured only part of the work
-    assert r0["local_calls"] + r1["local_calls"] == ref.evaluations_performed
+    # each rank measured only part of the work (speculative prefetch fills
+    # odd batches: world 2 = two slots per round; unused ones are counted)
+    assert r0["speculated_unused"] == r1["speculated_unused"]
+    assert r0["local_calls"] + r1["local_calls"] == ref.evaluations_performed + r0["speculated_unused"]
     assert r0["local_calls"] > 0 and r1["local_calls"] > 0
