@@ -22,6 +22,31 @@ def source(n: int = 1024) -> str:
     )
 
 
+def python_source(n: int = 1024) -> str:
+    """The same program as real Python (BASELINE config 1 is a *Python*
+    matmul app): lowered by frontends/python_src.py to the same IR as
+    :func:`source` (tests/test_frontends.py)."""
+    return (
+        '"""Naive matmul: the paper\'s Python loop-offload example shape."""\n'
+        "import numpy as np\n\n"
+        f"N = {n}\n"
+        "ma = np.zeros(N * N, dtype=np.float32)\n"
+        "mb = np.zeros(N * N, dtype=np.float32)\n"
+        "mc = np.zeros(N * N, dtype=np.float32)\n"
+        "chk = 0.0\n\n\n"
+        "def main():\n"
+        "    global chk\n"
+        "    for i in range(N):\n"
+        "        for j in range(N):\n"
+        "            mc[i * N + j] = 0.0\n"
+        "            for k in range(N):\n"
+        "                mc[i * N + j] = mc[i * N + j] + ma[i * N + k] * mb[k * N + j]\n"
+        "    chk = mc[0]\n\n\n"
+        'if __name__ == "__main__":\n'
+        "    main()\n"
+    )
+
+
 def spec(n: int = 1024, seed: int = 2011036021) -> dict:
     return {
         "name": f"matmul_{n}",
