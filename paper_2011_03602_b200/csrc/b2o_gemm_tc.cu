@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -284,6 +285,221 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// the CTA-pair kernel (cta_group::2): one 256 x 256 output tile per cluster
+// of two CTAs on one TPC.  Each CTA stages its own 128 rows of A and its own
+// 128 columns of B (hi and lo planes); the leader's single thread issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 8) that reads both CTAs'
+// shared memory and accumulates into both CTAs' TMEM (128 lanes x 256
+// columns each).  Per SM this halves the B operand traffic of the 1-CTA
+// kernel (shared-memory bandwidth was its limiter: ~158 B/clk of operand
+// reads + TMA writes against 128 B/clk), and gives 3 pipeline stages.
+//   both CTAs: warp 0 TMA producer (completes on the LEADER's full barrier),
+//              warps 2..9 epilogue (own TMEM, arrive on the leader's
+//              accumulator-empty barrier);
+//   leader:    warp 1 lane 0 MMA issuer, commits multicast to both CTAs.
+// ---------------------------------------------------------------------------
+
+namespace pair {
+
+constexpr int BM = 128, BN = 256, BNH = 128, BK = 32, STAGES = 3;
+constexpr int A_TILE = BM * BK * 4;                  // 16 KB
+constexpr int B_TILE = BNH * BK * 4;                 // 16 KB (this CTA's half of N)
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;  // 64 KB per CTA
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int KCHUNK_BLOCKS = 4;
+// D f32, A/B tf32, K-major, N = 256, M = 256 (pair)
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2sm(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  const uint16_t mask = 0x3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          bar),
+      "h"(mask)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                        const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                        float *__restrict__ C, int M, int N, int K) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+  // bars: full[STAGES], empty[STAGES], acc_full[2], acc_empty[2]; then the TMEM slot
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * STAGES + 4);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+  const uint32_t accf0 = smem_u32(bars + 2 * STAGES), acce0 = smem_u32(bars + 2 * STAGES + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair_id = blockIdx.x >> 1;
+  const int tiles_m = M / (2 * BM);
+  const int m0 = (pair_id % tiles_m) * (2 * BM) + (int)rank * BM;  // this CTA's 128 rows
+  const int n0 = (pair_id / tiles_m) * BN;                          // the pair's 256 columns
+  const int nb = n0 + (int)rank * BNH;                              // this CTA's half of B
+  const int kblocks = K / BK;
+  const int nchunks = (kblocks + KCHUNK_BLOCKS - 1) / KCHUNK_BLOCKS;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 2 * EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mAh) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mBh) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(empty0 + 8 * s, ph ^ 1);
+        uint8_t *st = smem + s * STAGE_BYTES;
+        const uint32_t fb_local = full0 + 8 * s;
+        if (leader) mbar_expect_tx(fb_local, 2 * STAGE_BYTES);  // both CTAs' bytes land on the leader
+        const uint32_t fb = map_to_rank(fb_local, 0);
+        tma_load_2sm(smem_u32(st), &mAh, kb * BK, m0, fb);
+        tma_load_2sm(smem_u32(st + A_TILE), &mAl, kb * BK, m0, fb);
+        tma_load_2sm(smem_u32(st + 2 * A_TILE), &mBh, kb * BK, nb, fb);
+        tma_load_2sm(smem_u32(st + 2 * A_TILE + B_TILE), &mBl, kb * BK, nb, fb);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c >= 2) mbar_wait(acce0 + 8 * buf, ((c - 2) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc_tmem = tmem + (uint32_t)(buf * BN);
+        const int kb_end = min(kblocks, (c + 1) * KCHUNK_BLOCKS);
+        for (int kb = c * KCHUNK_BLOCKS; kb < kb_end; ++kb) {
+          const int s = kb % STAGES;
+          const uint32_t ph = (kb / STAGES) & 1;
+          mbar_wait(full0 + 8 * s, ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a_h = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t a_l = a_h + A_TILE;
+          const uint32_t b_h = a_h + 2 * A_TILE;
+          const uint32_t b_l = b_h + B_TILE;
+          const bool first_kb = kb == c * KCHUNK_BLOCKS;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t off = kk * 8 * 4;
+            const uint32_t acc = (first_kb && kk == 0) ? 0u : 1u;
+            umma_tf32_pair(acc_tmem, smem_desc(a_l + off), smem_desc(b_h + off), acc);
+            umma_tf32_pair(acc_tmem, smem_desc(a_h + off), smem_desc(b_l + off), 1u);
+            umma_tf32_pair(acc_tmem, smem_desc(a_h + off), smem_desc(b_h + off), 1u);
+          }
+          umma_commit_pair(empty0 + 8 * s);  // frees stage s in BOTH CTAs
+        }
+        umma_commit_pair(accf0 + 8 * buf);
+      }
+    }
+  } else {
+    const int q = warp % 4;
+    const int h = (warp - 2) / 4;
+    const uint32_t acce_leader = map_to_rank(acce0, 0);
+    float sum[128];
+#pragma unroll
+    for (int j = 0; j < 128; ++j) sum[j] = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      mbar_wait(accf0 + 8 * buf, (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int part = 0; part < 4; ++part) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + part * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+              "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum[part * 32 + j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acce_leader + 8 * buf)
+                     : "memory");
+    }
+    const int row = m0 + q * 32 + lane;
+    float4 *dst = (float4 *)(C + (size_t)row * N + n0 + h * 128);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dst[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();  // the peer's last arrivals have landed; no MMA still targets either TMEM
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace pair
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 
@@ -356,12 +572,42 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
   dim3 tg((unsigned)(n / 32), (unsigned)(k / 32));
   split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bh, Bl, (int)k, (int)n);
   CUtensorMap mAh, mAl, mBh, mBl;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static const bool force_1cta = getenv("B2O_GEMM_1CTA") != nullptr;
+  if (m % (2 * pair::BM) == 0 && n % pair::BN == 0 && !force_1cta) {
+    // CTA pairs: each CTA maps 128 rows of A and 128 rows (= N columns) of B^T
+    if (!make_map(&mAh, Ah, (int)m, (int)k, pair::BM) || !make_map(&mAl, Al, (int)m, (int)k, pair::BM) ||
+        !make_map(&mBh, Bh, (int)n, (int)k, pair::BNH) || !make_map(&mBl, Bl, (int)n, (int)k, pair::BNH))
+      return -1;
+    static bool pattr[64] = {false};
+    if (!pattr[dev & 63]) {
+      if (cudaFuncSetAttribute(pair::gemm_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               pair::SMEM_BYTES) != cudaSuccess)
+        return -1;
+      pattr[dev & 63] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * (m / (2 * pair::BM)) * (n / pair::BN)));
+    cfg.blockDim = dim3(pair::THREADS);
+    cfg.dynamicSmemBytes = pair::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, pair::gemm_tc_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k) !=
+        cudaSuccess)
+      return -1;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   if (!make_map(&mAh, Ah, (int)m, (int)k, BM) || !make_map(&mAl, Al, (int)m, (int)k, BM) ||
       !make_map(&mBh, Bh, (int)n, (int)k, BN) || !make_map(&mBl, Bl, (int)n, (int)k, BN))
     return -1;
   static bool attr[64] = {false};
-  int dev = 0;
-  cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
     if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
       return -1;
