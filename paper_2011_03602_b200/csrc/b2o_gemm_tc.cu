@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
@@ -356,10 +357,34 @@ __device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+// Persistent schedule over P pairs: pair p owns tiles p, p + P, ... (whole
+// K), and the T mod P tail tiles are cut into S = 2 K-halves (when that
+// fits in P units) so the last wave is half as long; the two halves add
+// into a zeroed C with red.global.add (0 + a + b == 0 + b + a: deterministic).
+struct Sched {
+  int P, T, waves, rem, S, tiles_m, nchunks;
+  __device__ int items(int p) const { return waves + (p < rem * S ? 1 : 0); }
+  // work item i of pair p: tile, chunk range [c0, c1), red-add epilogue?
+  __device__ void item(int p, int i, int &tile, int &c0, int &c1, bool &red) const {
+    if (i < waves) {
+      tile = p + i * P;
+      c0 = 0;
+      c1 = nchunks;
+      red = false;
+    } else {
+      tile = waves * P + p / S;
+      const int sl = p % S;
+      c0 = sl * nchunks / S;
+      c1 = (sl + 1) * nchunks / S;
+      red = S > 1;
+    }
+  }
+};
+
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                         const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
-                        float *__restrict__ C, int M, int N, int K) {
+                        float *__restrict__ C, int M, int N, int K, Sched sc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
@@ -372,12 +397,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair_id = blockIdx.x >> 1;
-  const int tiles_m = M / (2 * BM);
-  const int m0 = (pair_id % tiles_m) * (2 * BM) + (int)rank * BM;  // this CTA's 128 rows
-  const int n0 = (pair_id / tiles_m) * BN;                          // the pair's 256 columns
-  const int nb = n0 + (int)rank * BNH;                              // this CTA's half of B
   const int kblocks = K / BK;
-  const int nchunks = (kblocks + KCHUNK_BLOCKS - 1) / KCHUNK_BLOCKS;
+  const int n_items = sc.items(pair_id);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -404,89 +425,120 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(empty0 + 8 * s, ph ^ 1);
-        uint8_t *st = smem + s * STAGE_BYTES;
-        const uint32_t fb_local = full0 + 8 * s;
-        if (leader) mbar_expect_tx(fb_local, 2 * STAGE_BYTES);  // both CTAs' bytes land on the leader
-        const uint32_t fb = map_to_rank(fb_local, 0);
-        tma_load_2sm(smem_u32(st), &mAh, kb * BK, m0, fb);
-        tma_load_2sm(smem_u32(st + A_TILE), &mAl, kb * BK, m0, fb);
-        tma_load_2sm(smem_u32(st + 2 * A_TILE), &mBh, kb * BK, nb, fb);
-        tma_load_2sm(smem_u32(st + 2 * A_TILE + B_TILE), &mBl, kb * BK, nb, fb);
+      int g = 0;  // k-block sequence number across work items (stage / phase)
+      for (int it = 0; it < n_items; ++it) {
+        int tile, c0, c1;
+        bool red;
+        sc.item(pair_id, it, tile, c0, c1, red);
+        const int m0 = (tile % sc.tiles_m) * (2 * BM) + (int)rank * BM;
+        const int nb = (tile / sc.tiles_m) * BN + (int)rank * BNH;
+        const int kb_end = min(kblocks, c1 * KCHUNK_BLOCKS);
+        for (int kb = c0 * KCHUNK_BLOCKS; kb < kb_end; ++kb, ++g) {
+          const int s = g % STAGES;
+          const uint32_t ph = (g / STAGES) & 1;
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          uint8_t *st = smem + s * STAGE_BYTES;
+          const uint32_t fb_local = full0 + 8 * s;
+          if (leader) mbar_expect_tx(fb_local, 2 * STAGE_BYTES);  // both CTAs' bytes land on the leader
+          const uint32_t fb = map_to_rank(fb_local, 0);
+          tma_load_2sm(smem_u32(st), &mAh, kb * BK, m0, fb);
+          tma_load_2sm(smem_u32(st + A_TILE), &mAl, kb * BK, m0, fb);
+          tma_load_2sm(smem_u32(st + 2 * A_TILE), &mBh, kb * BK, nb, fb);
+          tma_load_2sm(smem_u32(st + 2 * A_TILE + B_TILE), &mBl, kb * BK, nb, fb);
+        }
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        if (c >= 2) mbar_wait(acce0 + 8 * buf, ((c - 2) >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc_tmem = tmem + (uint32_t)(buf * BN);
-        const int kb_end = min(kblocks, (c + 1) * KCHUNK_BLOCKS);
-        for (int kb = c * KCHUNK_BLOCKS; kb < kb_end; ++kb) {
-          const int s = kb % STAGES;
-          const uint32_t ph = (kb / STAGES) & 1;
-          mbar_wait(full0 + 8 * s, ph);
+      int g = 0, gc = 0;
+      for (int it = 0; it < n_items; ++it) {
+        int tile, c0, c1;
+        bool red;
+        sc.item(pair_id, it, tile, c0, c1, red);
+        for (int c = c0; c < c1; ++c, ++gc) {
+          const int buf = gc & 1;
+          if (gc >= 2) mbar_wait(acce0 + 8 * buf, ((gc - 2) >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t a_h = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t a_l = a_h + A_TILE;
-          const uint32_t b_h = a_h + 2 * A_TILE;
-          const uint32_t b_l = b_h + B_TILE;
-          const bool first_kb = kb == c * KCHUNK_BLOCKS;
+          const uint32_t acc_tmem = tmem + (uint32_t)(buf * BN);
+          const int kb_end = min(kblocks, (c + 1) * KCHUNK_BLOCKS);
+          for (int kb = c * KCHUNK_BLOCKS; kb < kb_end; ++kb, ++g) {
+            const int s = g % STAGES;
+            const uint32_t ph = (g / STAGES) & 1;
+            mbar_wait(full0 + 8 * s, ph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t a_h = smem_u32(smem + s * STAGE_BYTES);
+            const uint32_t a_l = a_h + A_TILE;
+            const uint32_t b_h = a_h + 2 * A_TILE;
+            const uint32_t b_l = b_h + B_TILE;
+            const bool first_kb = kb == c * KCHUNK_BLOCKS;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t off = kk * 8 * 4;
-            const uint32_t acc = (first_kb && kk == 0) ? 0u : 1u;
-            umma_tf32_pair(acc_tmem, smem_desc(a_l + off), smem_desc(b_h + off), acc);
-            umma_tf32_pair(acc_tmem, smem_desc(a_h + off), smem_desc(b_l + off), 1u);
-            umma_tf32_pair(acc_tmem, smem_desc(a_h + off), smem_desc(b_h + off), 1u);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t off = kk * 8 * 4;
+              const uint32_t acc = (first_kb && kk == 0) ? 0u : 1u;
+              umma_tf32_pair(acc_tmem, smem_desc(a_l + off), smem_desc(b_h + off), acc);
+              umma_tf32_pair(acc_tmem, smem_desc(a_h + off), smem_desc(b_l + off), 1u);
+              umma_tf32_pair(acc_tmem, smem_desc(a_h + off), smem_desc(b_h + off), 1u);
+            }
+            umma_commit_pair(empty0 + 8 * s);  // frees stage s in BOTH CTAs
           }
-          umma_commit_pair(empty0 + 8 * s);  // frees stage s in BOTH CTAs
+          umma_commit_pair(accf0 + 8 * buf);
         }
-        umma_commit_pair(accf0 + 8 * buf);
       }
     }
   } else {
     const int q = warp % 4;
     const int h = (warp - 2) / 4;
     const uint32_t acce_leader = map_to_rank(acce0, 0);
-    float sum[128];
+    int gc = 0;
+    for (int it = 0; it < n_items; ++it) {
+      int tile, c0, c1;
+      bool red;
+      sc.item(pair_id, it, tile, c0, c1, red);
+      float sum[128];
 #pragma unroll
-    for (int j = 0; j < 128; ++j) sum[j] = 0.f;
-    for (int c = 0; c < nchunks; ++c) {
-      const int buf = c & 1;
-      mbar_wait(accf0 + 8 * buf, (c >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int j = 0; j < 128; ++j) sum[j] = 0.f;
+      for (int c = c0; c < c1; ++c, ++gc) {
+        const int buf = gc & 1;
+        mbar_wait(accf0 + 8 * buf, (gc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-      for (int part = 0; part < 4; ++part) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + part * 32);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
-              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-              "=r"(r[30]), "=r"(r[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int part = 0; part < 4; ++part) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * 128 + part * 32);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+              "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sum[part * 32 + j] += __uint_as_float(r[j]);
+          for (int j = 0; j < 32; ++j) sum[part * 32 + j] += __uint_as_float(r[j]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acce_leader + 8 * buf)
+                       : "memory");
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acce_leader + 8 * buf)
-                     : "memory");
-    }
-    const int row = m0 + q * 32 + lane;
-    float4 *dst = (float4 *)(C + (size_t)row * N + n0 + h * 128);
+      const int m0 = (tile % sc.tiles_m) * (2 * BM) + (int)rank * BM;
+      const int n0 = (tile / sc.tiles_m) * BN;
+      float *dst = C + (size_t)(m0 + q * 32 + lane) * N + n0 + h * 128;
+      if (!red) {
+        float4 *d4 = (float4 *)dst;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) dst[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+        for (int j = 0; j < 32; ++j) d4[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * j), "f"(sum[4 * j]),
+                       "f"(sum[4 * j + 1]), "f"(sum[4 * j + 2]), "f"(sum[4 * j + 3])
+                       : "memory");
+      }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -495,6 +547,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
+}
+
+// zero the K-split tail tiles before their halves red-add into them
+__global__ void zero_tiles_kernel(float *__restrict__ C, int N, int tiles_m, int first_tile) {
+  const int tile = first_tile + blockIdx.y;
+  const int m0 = (tile % tiles_m) * (2 * BM), n0 = (tile / tiles_m) * BN;
+  const int row = m0 + blockIdx.x;
+  float4 *d = (float4 *)(C + (size_t)row * N + n0);
+  for (int j = threadIdx.x; j < BN / 4; j += blockDim.x) d[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 }  // namespace pair
@@ -587,8 +648,21 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
         return -1;
       pattr[dev & 63] = true;
     }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    pair::Sched sc{};
+    sc.tiles_m = (int)(m / (2 * pair::BM));
+    sc.T = sc.tiles_m * (int)(n / pair::BN);
+    sc.P = std::max(1, std::min(sms / 2, sc.T));
+    sc.waves = sc.T / sc.P;
+    sc.rem = sc.T % sc.P;
+    sc.nchunks = (int)((k / pair::BK + pair::KCHUNK_BLOCKS - 1) / pair::KCHUNK_BLOCKS);
+    sc.S = (sc.rem > 0 && 2 * sc.rem <= sc.P && sc.nchunks >= 2 && !getenv("B2O_GEMM_NOSPLIT")) ? 2 : 1;
+    if (sc.S == 2) {
+      pair::zero_tiles_kernel<<<dim3(2 * pair::BM, sc.rem), 64, 0, s>>>(C, (int)n, sc.tiles_m, sc.waves * sc.P);
+    }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * (m / (2 * pair::BM)) * (n / pair::BN)));
+    cfg.gridDim = dim3((unsigned)(2 * sc.P));
     cfg.blockDim = dim3(pair::THREADS);
     cfg.dynamicSmemBytes = pair::SMEM_BYTES;
     cfg.stream = s;
@@ -599,7 +673,7 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, pair::gemm_tc_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k) !=
+    if (cudaLaunchKernelEx(&cfg, pair::gemm_tc_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k, sc) !=
         cudaSuccess)
       return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;

@@ -32,7 +32,8 @@ def _gemm(torch, m, n, k, seed=0, lo=0.0):
     return c.double().cpu().numpy(), ref
 
 
-@pytest.mark.parametrize("m,n,k", [(128, 256, 32), (256, 512, 96), (1024, 1024, 1024), (4096, 4096, 4096)])
+@pytest.mark.parametrize("m,n,k", [(128, 256, 32), (256, 512, 96), (1024, 1024, 1024), (2560, 2560, 512),
+                                   (3072, 4096, 1024), (4096, 4096, 4096)])
 def test_tcgen05_gemm_matches_float64(torch_cuda, m, n, k):
     from paper_2011_03602_b200.runtime import lib
 
@@ -72,3 +73,21 @@ def test_fft2d_matches_numpy(torch_cuda, n):
     y = dy.cpu().numpy().astype(np.float64).reshape(n, n, 2)
     got = y[..., 0] + 1j * y[..., 1]
     assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-5
+
+
+def test_gemm_deterministic_with_split_tail(torch_cuda):
+    """The K-split tail tiles add their two halves into a zeroed C: 0 + a + b
+    equals 0 + b + a in IEEE arithmetic, so repeated runs are bit-identical."""
+    from paper_2011_03602_b200.runtime import lib
+
+    torch = torch_cuda
+    g = torch.Generator(device="cpu").manual_seed(11)
+    a = torch.rand(2560, 512, generator=g).cuda()
+    b = torch.rand(512, 2560, generator=g).cuda()
+    outs = []
+    for _ in range(3):
+        c = torch.full((2560, 2560), float("nan"), device="cuda")
+        assert lib().b2o_gemm_f32(a.data_ptr(), b.data_ptr(), c.data_ptr(), 2560, 2560, 512,
+                                  torch.cuda.current_stream().cuda_stream) == 0
+        outs.append(c.cpu())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
