@@ -120,30 +120,48 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
 // operand preparation: hi/lo split (A), split + transpose (B)
 // ---------------------------------------------------------------------------
 
-__global__ void split_kernel(const float *__restrict__ x, float *__restrict__ hi, float *__restrict__ lo, size_t n) {
+// mode 0: hi = rna_tf32(x), lo = rna_tf32(x - hi)   (the production split)
+// mode 1: hi = x, lo = 0                              (probe: what the tensor core does with raw fp32)
+// mode 2: hi = x, lo = rna_tf32(x - trunc_tf32(x))   (split for the truncating tensor core:
+//         tcgen05 kind::tf32 drops the low 13 bits, tools/tf32_probe.py)
+__device__ __forceinline__ void split_value(float v, int mode, float &h, float &l) {
+  if (mode == 0) {
+    h = __uint_as_float(tf32_rna(v));
+    l = __uint_as_float(tf32_rna(v - h));
+  } else if (mode == 1) {
+    h = v;
+    l = 0.f;
+  } else {
+    h = v;
+    l = __uint_as_float(tf32_rna(v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u)));
+  }
+}
+
+__global__ void split_kernel(const float *__restrict__ x, float *__restrict__ hi, float *__restrict__ lo, size_t n,
+                             int mode) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
-    float v = x[i];
-    float h = __uint_as_float(tf32_rna(v));
+    float h, l;
+    split_value(x[i], mode, h, l);
     hi[i] = h;
-    lo[i] = __uint_as_float(tf32_rna(v - h));
+    lo[i] = l;
   }
 }
 
 // B is K x N row-major; write BhT/BlT as N x K row-major (K-major operand)
 __global__ void split_transpose_kernel(const float *__restrict__ b, float *__restrict__ hiT, float *__restrict__ loT,
-                                       int K, int N) {
+                                       int K, int N, int mode) {
   __shared__ float tile[32][33];
   const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) tile[r][threadIdx.x] = b[(size_t)(k0 + r) * N + n0 + threadIdx.x];
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    float v = tile[threadIdx.x][r];
-    float h = __uint_as_float(tf32_rna(v));
+    float h, l;
+    split_value(tile[threadIdx.x][r], mode, h, l);
     size_t o = (size_t)(n0 + r) * K + k0 + threadIdx.x;
     hiT[o] = h;
-    loT[o] = __uint_as_float(tf32_rna(v - h));
+    loT[o] = l;
   }
 }
 
@@ -629,9 +647,10 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
   float *ws = workspace(sizeof(float) * 2 * (a_elems + b_elems));
   if (!ws) return -1;
   float *Ah = ws, *Al = ws + a_elems, *Bh = Al + a_elems, *Bl = Bh + b_elems;
-  split_kernel<<<148 * 8, 256, 0, s>>>(A, Ah, Al, a_elems);
+  static const int split_mode = getenv("B2O_GEMM_SPLIT") ? atoi(getenv("B2O_GEMM_SPLIT")) : 0;
+  split_kernel<<<148 * 8, 256, 0, s>>>(A, Ah, Al, a_elems, split_mode);
   dim3 tg((unsigned)(n / 32), (unsigned)(k / 32));
-  split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bh, Bl, (int)k, (int)n);
+  split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bh, Bl, (int)k, (int)n, split_mode);
   CUtensorMap mAh, mAl, mBh, mBl;
   int dev = 0;
   cudaGetDevice(&dev);
