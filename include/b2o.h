@@ -132,6 +132,10 @@ int b2o_bench_replay(uint64_t app, int32_t worker, const b2o_pattern *pattern, i
 int b2o_gemm_f32(const float *A, const float *B, float *C, int64_t m, int64_t n, int64_t k, void *stream);
 int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream);
 int b2o_gemm_impl(void);  /* which GEMM path the build uses: 1 = tcgen05 3xTF32, 0 = SIMT */
+/* measurement hook: b2o_gemm_f32 on the tcgen05 path (-2 if the shape does not
+ * tile) plus device ms of operand preparation and of the MMA kernel; synchronises */
+int b2o_gemm_f32_phases(const float *A, const float *B, float *C, int64_t m, int64_t n, int64_t k, void *stream,
+                        double *prep_ms, double *mma_ms);
 /* h[d[i]] += 1 for i < n on the device (values outside [0, bins) skipped);
  * elem: element type of h, 0 = int32, 1 = fp32, 2 = fp64 (b2o_module.h b2o_elem) */
 int b2o_histogram(const int32_t *d, int64_t n, void *h, int64_t bins, int elem, void *stream);

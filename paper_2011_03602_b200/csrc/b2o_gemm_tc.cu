@@ -636,6 +636,10 @@ float *workspace(size_t bytes) {
 extern "C" int b2o_gemm_impl(void) { return 1; }
 
 // returns -2 when the shape does not tile (caller falls back to SIMT)
+// measurement hook (b2o_gemm_f32_phases): events around operand prep and the MMA kernel
+std::mutex phase_mu;
+cudaEvent_t *phase_ev = nullptr;
+
 extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t m, int64_t n, int64_t k,
                                void *stream) {
   if (m % BM || n % BN || k % BK || m <= 0 || n <= 0 || k <= 0 || m > (1 << 20) || n > (1 << 20) ||
@@ -648,9 +652,11 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
   if (!ws) return -1;
   float *Ah = ws, *Al = ws + a_elems, *Bh = Al + a_elems, *Bl = Bh + b_elems;
   static const int split_mode = getenv("B2O_GEMM_SPLIT") ? atoi(getenv("B2O_GEMM_SPLIT")) : 0;
+  if (phase_ev) cudaEventRecord(phase_ev[0], s);
   split_kernel<<<148 * 8, 256, 0, s>>>(A, Ah, Al, a_elems, split_mode);
   dim3 tg((unsigned)(n / 32), (unsigned)(k / 32));
   split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bh, Bl, (int)k, (int)n, split_mode);
+  if (phase_ev) cudaEventRecord(phase_ev[1], s);
   CUtensorMap mAh, mAl, mBh, mBl;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -695,6 +701,7 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
     if (cudaLaunchKernelEx(&cfg, pair::gemm_tc_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k, sc) !=
         cudaSuccess)
       return -1;
+    if (phase_ev) cudaEventRecord(phase_ev[2], s);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
   if (!make_map(&mAh, Ah, (int)m, (int)k, BM) || !make_map(&mAl, Al, (int)m, (int)k, BM) ||
@@ -709,4 +716,27 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
   const unsigned tiles = (unsigned)((m / BM) * (n / BN));
   gemm_tc_kernel<<<tiles, THREADS, SMEM_BYTES, s>>>(mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// C = A B like b2o_gemm_f32 (tcgen05 path only), plus the device time of the
+// operand preparation and of the MMA kernel (CUDA events on `stream`; the
+// call synchronises).  Measurement hook for bench.py's roofline.
+extern "C" int b2o_gemm_f32_phases(const float *A, const float *B, float *C, int64_t m, int64_t n, int64_t k,
+                                   void *stream, double *prep_ms, double *mma_ms) {
+  std::lock_guard<std::mutex> lk(phase_mu);
+  cudaEvent_t ev[3];
+  for (auto &e : ev) cudaEventCreate(&e);
+  phase_ev = ev;
+  int rc = b2o_gemm_tc_f32(A, B, C, m, n, k, stream);
+  phase_ev = nullptr;
+  if (rc == 0) {
+    cudaEventSynchronize(ev[2]);
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    if (prep_ms) *prep_ms = a;
+    if (mma_ms) *mma_ms = b;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  return rc;
 }

@@ -104,6 +104,8 @@ def lib() -> ctypes.CDLL:
             "b2o_wait": ([ctypes.c_uint64, ctypes.POINTER(Result), ctypes.c_int32, ctypes.c_double], ctypes.c_int),
             "b2o_gemm_f32": ([ctypes.c_void_p] * 3 + [ctypes.c_int64] * 3 + [ctypes.c_void_p], ctypes.c_int),
             "b2o_fft2d_c64": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p], ctypes.c_int),
+            "b2o_gemm_f32_phases": ([ctypes.c_void_p] * 3 + [ctypes.c_int64] * 3 + [ctypes.c_void_p] * 3,
+                                    ctypes.c_int),
             "b2o_histogram": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                ctypes.c_void_p], ctypes.c_int),
             "b2o_gemm_impl": ([], ctypes.c_int),
