@@ -619,6 +619,41 @@ std::string configure_pattern(AppDev *d, const Job &j) {
   return "";
 }
 
+// the reference rule |c - r| <= max(rel * |r|, 1e-12) (src/evaluators.py:129-139)
+// per element, typed so the loops vectorise; returns (mismatches, worst rel)
+template <typename T>
+void compare_elementwise(const T *cand, const T *ref, int64_t n, double tol, uint64_t &bad, double &worst) {
+  uint64_t cnt = 0;
+  double worst_local = 0.0;
+  bool saw_nan = false;
+  const int nthr = n > (1 << 18) ? 16 : 1;
+#pragma omp parallel for num_threads(nthr) reduction(+ : cnt) reduction(max : worst_local) reduction(|| : saw_nan) schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double c = (double)cand[i], rr = (double)ref[i];
+    const double diff = std::fabs(c - rr);
+    const double ar = std::fabs(rr);
+    cnt += !(diff <= std::max(tol * ar, 1e-12));
+    const double rel = diff / std::max(ar, 1e-30);
+    saw_nan = saw_nan || (rel != rel);
+    worst_local = rel > worst_local ? rel : worst_local;
+  }
+  bad = cnt;
+  worst = saw_nan ? INFINITY : worst_local;
+}
+
+template <typename T>
+double normwise_rel(const T *cand, const T *ref, int64_t n) {
+  double num = 0.0, den = 0.0;
+  const int nthr = n > (1 << 18) ? 16 : 1;
+#pragma omp parallel for num_threads(nthr) reduction(+ : num, den) schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double c = (double)cand[i], rr = (double)ref[i];
+    num += (c - rr) * (c - rr);
+    den += rr * rr;
+  }
+  return std::sqrt(num) / std::max(std::sqrt(den), 1e-300);
+}
+
 void compare_outputs(AppDev *d, b2o_result &r) {
   AppShared *a = d->app;
   const b2o_module_info *info = a->info;
@@ -631,43 +666,22 @@ void compare_outputs(AppDev *d, b2o_result &r) {
     if (it == a->reference.end()) continue;
     const b2o_var_info &vi = info->vars[oi.var];
     int64_t n = vi.is_array ? vi.length : 1;
-    const char *cand = (const char *)d->host[oi.var];
-    const char *ref = it->second.data();
-    auto val = [&](const char *base, int64_t i) -> double {
-      if (vi.elem == B2O_I32) return (double)((const int32_t *)base)[i];
-      if (vi.elem == B2O_F32) return (double)((const float *)base)[i];
-      return ((const double *)base)[i];
-    };
+    const void *cand = d->host[oi.var];
+    const void *ref = it->second.data();
     uint64_t nbad = 0;
     double w = 0.0;
-    const int nthr = n > (1 << 20) ? 8 : 1;
     if (oi.mode == B2O_CMP_NORMWISE) {
-      double num = 0.0, den = 0.0;
-#pragma omp parallel for num_threads(nthr) reduction(+ : num, den) schedule(static)
-      for (int64_t i = 0; i < n; ++i) {
-        double c = val(cand, i), rr = val(ref, i);
-        num += (c - rr) * (c - rr);
-        den += rr * rr;
-      }
-      double rel = std::sqrt(num) / std::max(std::sqrt(den), 1e-300);
+      double rel = vi.elem == B2O_I32   ? normwise_rel((const int32_t *)cand, (const int32_t *)ref, n)
+                   : vi.elem == B2O_F32 ? normwise_rel((const float *)cand, (const float *)ref, n)
+                                        : normwise_rel((const double *)cand, (const double *)ref, n);
       if (!(rel <= oi.rel_tol)) nbad = 1;
       w = rel;
+    } else if (vi.elem == B2O_I32) {
+      compare_elementwise((const int32_t *)cand, (const int32_t *)ref, n, oi.rel_tol, nbad, w);
+    } else if (vi.elem == B2O_F32) {
+      compare_elementwise((const float *)cand, (const float *)ref, n, oi.rel_tol, nbad, w);
     } else {
-      const double tol = oi.rel_tol;
-      uint64_t cnt = 0;
-      double worst_local = 0.0;
-      bool saw_nan = false;
-#pragma omp parallel for num_threads(nthr) reduction(+ : cnt) reduction(max : worst_local) reduction(|| : saw_nan) schedule(static)
-      for (int64_t i = 0; i < n; ++i) {
-        double c = val(cand, i), rr = val(ref, i);
-        double diff = std::fabs(c - rr);
-        if (!(diff <= std::max(tol * std::fabs(rr), 1e-12))) ++cnt;
-        double rel = diff / std::max(std::fabs(rr), 1e-30);
-        if (std::isnan(rel)) saw_nan = true;
-        else if (rel > worst_local) worst_local = rel;
-      }
-      nbad = cnt;
-      w = saw_nan ? INFINITY : worst_local;
+      compare_elementwise((const double *)cand, (const double *)ref, n, oi.rel_tol, nbad, w);
     }
     worst = std::max(worst, w);
     if (nbad && first_bad.empty()) first_bad = vi.name;
@@ -708,8 +722,13 @@ void execute(Worker *w, Job &j) {
   int reps = std::max(1, j.pat.repeats);
   double best = INFINITY;
   b2o_result keep{};
+  static const bool trace = getenv("B2O_TRACE") != nullptr;
+  auto tr0 = Clock::now();
+  double reset_ms = 0.0;
   for (int rep = 0; rep < reps; ++rep) {
+    auto tr = Clock::now();
     reset_state(d);
+    reset_ms += std::chrono::duration<double, std::milli>(Clock::now() - tr).count();
     w->timed_out = 0;
     w->deadline_ns = j.pat.timeout_s > 0 ? now_ns() + (int64_t)(j.pat.timeout_s * 1e9) : 0;
     w->running = &d->ex;
@@ -756,8 +775,17 @@ void execute(Worker *w, Job &j) {
     snprintf(r.diag, sizeof r.diag, "%s", d->err.c_str());
     return;
   }
+  auto tc = Clock::now();
   compare_outputs(d, r);
   d->have_final = true;
+  if (trace) {
+    auto te = Clock::now();
+    fprintf(stderr, "[b2o] job worker=%d reset %.3f ms, run %.3f ms, fetch+compare %.3f ms (compare %.3f), total %.3f ms\n",
+            w->index, reset_ms, best * 1e3,
+            std::chrono::duration<double, std::milli>(te - tr0).count() - reset_ms - best * 1e3 * reps,
+            std::chrono::duration<double, std::milli>(te - tc).count(),
+            std::chrono::duration<double, std::milli>(te - tr0).count());
+  }
 }
 
 void worker_loop(Worker *w) {

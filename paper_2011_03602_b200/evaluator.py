@@ -119,6 +119,7 @@ class B200Evaluator:
         self._apps: dict[str, NativeApp | Exception] = {}
         self._families: dict[str, dict[str, np.ndarray]] = {}
         self._docs: dict[int, tuple[object, dict]] = {}
+        self._keys: dict[int, tuple[dict, str]] = {}
         self.log: list[dict] = []
 
     @property
@@ -139,9 +140,19 @@ class B200Evaluator:
         self._docs[id(model)] = (model, doc)
         return doc
 
+    def _key(self, doc: dict) -> str:
+        """build_key (a sha256 over the whole document) memoised per document
+        object: the GA and the bench hand the same dict over and over."""
+        hit = self._keys.get(id(doc))
+        if hit is not None and hit[0] is doc:
+            return hit[1]
+        key = build_key(doc, self.spec)
+        self._keys[id(doc)] = (doc, key)
+        return key
+
     def app_for(self, doc: dict) -> NativeApp:
         """Compile + load (cached). Raises CompileError / B2OError."""
-        key = build_key(doc, self.spec)
+        key = self._key(doc)
         got = self._apps.get(key)
         if isinstance(got, Exception):
             raise got
