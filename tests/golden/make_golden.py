@@ -213,6 +213,15 @@ def main() -> None:
         rec = app_record(name, m, spec, extra_genomes=extra, screen=screen_model_with_reductions,
                          all_genomes_cap=64 if not extra else 1)
         (HERE / f"{name}.json").write_text(json.dumps(rec, sort_keys=True) + "\n")
+    # differential fuzz programs (tests/_fuzz.py): all genomes, reference plans
+    sys.path.insert(0, str(HERE.parent))
+    import _fuzz
+
+    fuzz = {}
+    for seed in _fuzz.SEEDS:
+        m = parse_mini_source(_fuzz.program(seed))
+        fuzz[str(seed)] = app_record(f"fuzz_{seed}", m, _fuzz.spec(seed), all_genomes_cap=256)
+    (HERE / "fuzz.json").write_text(json.dumps(fuzz, sort_keys=True) + "\n")
     print("wrote", sorted(p.name for p in HERE.glob("*.json")))
 
 
