@@ -154,13 +154,23 @@ __global__ void __launch_bounds__(kHistThreads) hist_smem_kernel(const int32_t *
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n4 = (((uintptr_t)d & 15) == 0) ? n / 4 : 0;
   const int4 *d4 = (const int4 *)d;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    const int4 q = __ldcs(d4 + i);  // streamed once: evict-first
+  auto count4 = [&](const int4 q) {
     if ((uint32_t)q.x < ub) atomicAdd(&mine[q.x], 1u);
     if ((uint32_t)q.y < ub) atomicAdd(&mine[q.y], 1u);
     if ((uint32_t)q.z < ub) atomicAdd(&mine[q.z], 1u);
     if ((uint32_t)q.w < ub) atomicAdd(&mine[q.w], 1u);
+  };
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // four independent 16-byte loads in flight per thread before the atomics
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    const int4 q0 = __ldcs(d4 + i), q1 = __ldcs(d4 + i + stride), q2 = __ldcs(d4 + i + 2 * stride),
+               q3 = __ldcs(d4 + i + 3 * stride);  // streamed once: evict-first
+    count4(q0);
+    count4(q1);
+    count4(q2);
+    count4(q3);
   }
+  for (; i < n4; i += stride) count4(__ldcs(d4 + i));
   for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int32_t v = d[i];
     if ((uint32_t)v < ub) atomicAdd(&mine[v], 1u);
