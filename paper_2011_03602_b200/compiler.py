@@ -42,9 +42,13 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-16"
+COMPILER_VERSION = "b2o-compiler-21"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
+# plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
+# 258^3: 67.6 -> 53.4 us; tools/kernel_sweep.py, profiles/r01/README.md)
+MARCH_Z = 8
+MARCH_BLOCK = 128
 STENCIL_TILE = (32, 8)      # (k, j) tile of the 2.5-D stencil kernels
 BRICK_DEPTH = 4             # outer-loop points per thread in brick kernels
 
@@ -342,6 +346,44 @@ def quad_plan(prog: Program, chain: list[int], precision: str) -> dict | None:
     return {"outer": outer, "ovars": ovars, "ivs": sorted(ivs), "reads": reads, "writes": writes}
 
 
+def march_plan(prog: Program, chain: list[int], qp: dict, Z: int) -> dict | None:
+    """Plane-marching eligibility for a quad nest: at least two chain loops,
+    the outermost chain index enters every reference with one coefficient
+    ``C0`` that is a multiple of the quad (so a quad keeps its lanes from
+    plane to plane), and every reference constant splits uniquely into
+    ``d * C0 + rest`` with ``|rest| < C0 / 2 - QUAD``.  Returns
+    ``{"Z", "C0", "keys": {(array, d, chunk)}, "split"}`` or None."""
+    if len(chain) < 2 or Z < 2:
+        return None
+    iv0 = prog.loops[chain[0]].index_var
+    if not qp["ovars"] or qp["ovars"][0] != iv0:
+        return None
+    C0 = qp["outer"][0]
+    if C0 <= 0 or C0 % QUAD:
+        return None
+
+    def split(c):
+        d = (c + C0 // 2) // C0
+        return d, c - d * C0
+
+    keys = set()
+    for v, c in qp["reads"]:
+        d, rest = split(c)
+        if abs(rest) >= C0 // 2 - QUAD:
+            return None
+        if v in qp["writes"] and d != 0:
+            return None
+        for u in range(QUAD):
+            keys.add((v, d, (rest + u) // QUAD))
+    for v, c in qp["writes"].items():
+        d, rest = split(c)
+        if d != 0 or abs(rest) >= C0 // 2 - QUAD:
+            return None
+    if not any((v, d + 1, o) in keys and v not in qp["writes"] for v, d, o in keys):
+        return None  # nothing to carry from plane to plane: the plain quad kernel wins
+    return {"Z": Z, "C0": C0, "keys": keys, "split": split}
+
+
 def _first_access_is_read(prog: Program, lid: int, vid: int) -> bool:
     """Walk the nest in execution order of one thread's first iteration; True
     when ``vid`` may be read before any write (conservative)."""
@@ -470,6 +512,8 @@ class _Gen:
                     qp = quad_plan(prog, nst.chain, self.precision)
                     if qp is not None:
                         qp["groups"] = int(spec.get("quad_groups", 1))
+                        if qp["groups"] == 1 and not spec.get("quad_shfl"):
+                            qp["march"] = march_plan(prog, nst.chain, qp, int(spec.get("quad_march", MARCH_Z)))
                         nst.shape, nst.quad, nst.ppt = "quad", qp, 1
         self.device_op = {}
         for l in prog.loops:
@@ -702,6 +746,9 @@ class _Gen:
                 # its aligned chunk, so one extra (possibly empty) quad
                 L = QUAD * n.quad["groups"]
                 out.append(f"  a.tn[{D - 1}] = (a.n[{D - 1}] + {QUAD - 1 + L - 1}) / {L};")
+                if n.quad.get("march"):
+                    Z = n.quad["march"]["Z"]
+                    out.append(f"  a.tn[0] = (a.n[0] + {Z - 1}) / {Z};")
                 out.append("  total = 1;")
                 out.append(f"  for (int d = 0; d < {D}; ++d) total *= a.tn[d];")
             if n.kb > 1:
@@ -732,12 +779,15 @@ class _Gen:
             out.append(f"    geom[0] = tx; geom[1] = ty; geom[2] = (a.n[0] + a.chunk - 1) / a.chunk; "
                        f"geom[3] = {tk}; geom[4] = {tj}; geom[5] = 1; }}")
         else:
-            per = BLOCK_THREADS * n.ppt
+            bt = BLOCK_THREADS
+            if n.shape == "quad" and n.quad.get("march"):
+                bt = int(self.spec.get("march_block", MARCH_BLOCK))
+            per = bt * n.ppt
             cap = int(self.spec.get("flat_grid_cap", 0)) or 0x7FFFFFFF
             if n.reds:
                 cap = min(cap, 2048)  # B2O_RED_MAX_BLOCKS: one partial per CTA in the scratch
             out.append(f"  {{ uint64_t g = (total + {per - 1}) / {per}; geom[0] = (uint32_t)(g > {cap}u ? "
-                       f"{cap}u : g); geom[1] = geom[2] = 1; geom[3] = {BLOCK_THREADS}; geom[4] = geom[5] = 1; }}")
+                       f"{cap}u : g); geom[1] = geom[2] = 1; geom[3] = {bt}; geom[4] = geom[5] = 1; }}")
         out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, geom);")
         out.append("}")
         return out
@@ -770,6 +820,8 @@ class _Gen:
             return self.stencil_kernel_fn(n)
         if n.shape == "brick":
             return self.brick_kernel_fn(n)
+        if n.shape == "quad" and n.quad.get("march"):
+            return self.quad_march_kernel_fn(n)
         if n.shape == "quad":
             return self.quad_kernel_fn(n)
         prog = self.prog
@@ -910,12 +962,30 @@ class _Gen:
             const = "const " if v not in n.writes else ""
             out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
         out.extend(self._locals(n, "  "))
+        G = qp["groups"]
+        # warp-shuffle neighbour exchange (one quad per thread only): adjacent
+        # lanes own adjacent aligned chunks of a row, so of a run of chunks
+        # {o-1, o, o+1} a thread loads o and takes the lanes it needs of o-1 /
+        # o+1 from lanes -1 / +1; lanes whose neighbour sits in another row,
+        # another warp or is idle load those elements directly
+        shfl = G == 1 and bool(self.spec.get("quad_shfl", False))  # measured slower
         out.append("  const uint32_t stride = gridDim.x * blockDim.x;")
-        out.append("  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {")
-        out.append("    if (t == a.total - 1u) {")
-        out.extend(self._finals(n, "      "))
-        out.append("    }")
-        out.append("    uint32_t r = t;")
+        if shfl:
+            out.append("  const uint32_t lane_ = threadIdx.x & 31u;")
+            out.append("  for (uint32_t tw_ = blockIdx.x * blockDim.x + threadIdx.x - lane_; tw_ < a.total; "
+                       "tw_ += stride) {")
+            out.append("    const uint32_t t = tw_ + lane_;")
+            out.append("    const bool act_ = t < a.total;")
+            out.append("    if (t == a.total - 1u) {")
+            out.extend(self._finals(n, "      "))
+            out.append("    }")
+            out.append("    uint32_t r = act_ ? t : a.total - 1u;")
+        else:
+            out.append("  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {")
+            out.append("    if (t == a.total - 1u) {")
+            out.extend(self._finals(n, "      "))
+            out.append("    }")
+            out.append("    uint32_t r = t;")
         for d in range(D - 1, 0, -1):
             nm = "q_" if d == D - 1 else f"v{iv[d]}_"
             out.append(f"    uint32_t {nm};")
@@ -928,25 +998,90 @@ class _Gen:
             out.append(f"    const int32_t v{iv[d]} = a.lo[{d}] + (int32_t)v{iv[d]}_;")
         row = [f"(int64_t){c} * v{v}" for v, c in zip(qp["ovars"], qp["outer"]) if c]
         out.append(f"    const int64_t F_ = {' + '.join(row) if row else '0'};")
-        G = qp["groups"]
         L = QUAD * G  # lanes (points) per thread: G aligned quads of one row
         out.append(f"    const int64_t b_ = ((F_ + a.lo[{D - 1}]) & ~(int64_t){QUAD - 1}) + (int64_t){L} * q_;")
         out.append(f"    const int32_t k0_ = (int32_t)(b_ - F_);")
         out.append(f"    const int32_t kr_ = k0_ - a.lo[{D - 1}];")
         out.append(f"    const int32_t kn_ = (int32_t)a.n[{D - 1}];")
-        out.append(f"    if (kr_ + {L - 1} < 0 || kr_ >= kn_) continue;")
-        # aligned chunks every read needs
-        chunks = sorted({(v, (c + u) // QUAD) for v, c in qp["reads"] for u in range(L)})
+        if not shfl:
+            out.append(f"    if (kr_ + {L - 1} < 0 || kr_ >= kn_) continue;")
+        else:
+            out.append(f"    const bool ok_ = act_ && !(kr_ + {L - 1} < 0 || kr_ >= kn_);")
+        # aligned chunks every read needs, and the lanes used of each
+        comps: dict = {}
+        for v, c in qp["reads"]:
+            for u in range(L):
+                comps.setdefault((v, (c + u) // QUAD), set()).add((c + u) % QUAD)
+        chunks = sorted(comps)
 
         def cname(v, o):
             return f"c{v}_{'m' if o < 0 else ''}{abs(o)}"
 
-        for v, o in chunks:
+        def ldexpr(v, o):
             vt = "float4" if self.T(v) == "float" else "int4"
-            ld = "__ldg" if v not in qp["writes"] else ""  # read-only path only for arrays the nest never writes
-            out.append(f"    const {vt} {cname(v, o)} = {ld}(reinterpret_cast<const {vt} *>(v{v} + b_)[{o}]);"
-                       if not ld else
-                       f"    const {vt} {cname(v, o)} = __ldg(reinterpret_cast<const {vt} *>(v{v} + b_) + ({o}));")
+            if v in qp["writes"]:  # read-only path only for arrays the nest never writes
+                return f"(reinterpret_cast<const {vt} *>(v{v} + b_)[{o}])"
+            return f"__ldg(reinterpret_cast<const {vt} *>(v{v} + b_) + ({o}))"
+
+        shuffled: set = set()  # chunks held as per-lane scalars taken from neighbours
+        if not shfl:
+            for v, o in chunks:
+                vt = "float4" if self.T(v) == "float" else "int4"
+                out.append(f"    const {vt} {cname(v, o)} = {ldexpr(v, o)};")
+        else:
+            out.append("    const unsigned vm_ = __ballot_sync(0xffffffffu, ok_);")
+            out.append("    const uint32_t bl_ = (uint32_t)b_;")
+            # runs of consecutive chunks per array: load the middle one
+            runs: list = []
+            for v, o in chunks:
+                if runs and runs[-1][0] == v and runs[-1][-1] == o - 1:
+                    runs[-1].append(o)
+                else:
+                    runs.append([v, o])
+            # the centre is the chunk with the most lanes used (ties: the
+            # middle one); a neighbour chunk of which more than quad_shfl_max
+            # lanes are needed is loaded rather than shuffled
+            smax = int(self.spec.get("quad_shfl_max", 2))
+            deltas = set()
+            centres = {}
+            loaded: list = []
+            for run in runs:
+                v, os_ = run[0], run[1:]
+                mid = os_[len(os_) // 2]
+                oc = max(os_, key=lambda o: (len(comps[(v, o)]), -abs(o - mid)))
+                loaded.append((v, oc))
+                for o in os_:
+                    if o == oc:
+                        continue
+                    if len(comps[(v, o)]) > smax or abs(o - oc) > 1:
+                        loaded.append((v, o))
+                    else:
+                        centres[(v, o)] = oc
+                        deltas.add(o - oc)
+            for dl in sorted(deltas):
+                nm = f"nb{'m' if dl < 0 else ''}{abs(dl)}_"
+                # the shuffle runs on every lane (never behind a short-circuit)
+                out.append(f"    const uint32_t {nm}b = __shfl_sync(0xffffffffu, bl_, (lane_ + ({dl})) & 31u);")
+                out.append(f"    const bool {nm} = (lane_ + ({dl})) < 32u && ((vm_ >> ((lane_ + ({dl})) & 31u)) & 1u) "
+                           f"&& {nm}b == bl_ + {QUAD * dl}u;")
+            for v, o in sorted(loaded):
+                vt = "float4" if self.T(v) == "float" else "int4"
+                zero = "make_float4(0.f, 0.f, 0.f, 0.f)" if vt == "float4" else "make_int4(0, 0, 0, 0)"
+                out.append(f"    {vt} {cname(v, o)} = {zero};")
+                out.append(f"    if (ok_) {cname(v, o)} = {ldexpr(v, o)};")
+            for (v, o), oc in sorted(centres.items()):
+                T = self.T(v)
+                dl = o - oc
+                nm = f"nb{'m' if dl < 0 else ''}{abs(dl)}_"
+                shuffled.add((v, o))
+                for j in sorted(comps[(v, o)]):
+                    x = f"{cname(v, o)}_{j}"
+                    out.append(f"    {T} {x} = __shfl_sync(0xffffffffu, {cname(v, oc)}.{'xyzw'[j]}, "
+                               f"(lane_ + ({dl})) & 31u);")
+                    ptr = f"v{v} + b_ + ({QUAD * o + j})"
+                    src = f"__ldg({ptr})" if v not in qp["writes"] else f"*({ptr})"
+                    out.append(f"    if (!{nm} && ok_) {x} = {src};")
+            out.append("    if (!ok_) continue;")
         ivs = set(qp["ivs"])
 
         latest: dict[int, int] = {}  # array -> statement whose lane values it now holds
@@ -958,6 +1093,8 @@ class _Gen:
             if k == "arr":
                 c = affine(e[2], ivs)[1]
                 el = c + u
+                if (e[1], el // QUAD) in shuffled:
+                    return f"{cname(e[1], el // QUAD)}_{el % QUAD}"
                 return f"{cname(e[1], el // QUAD)}.{'xyzw'[el % QUAD]}"
             if k == "var" and e[1] == kv:
                 return f"(k0_ + {u})"
@@ -992,6 +1129,147 @@ class _Gen:
                     out.append("    {")
                     out.extend(masked)
                     out.append("    }")
+        for v in n.locals_:
+            out.append(f"    (void)v{v};")
+        out.append("  }")
+        out.append("}")
+        return out
+
+    def quad_march_kernel_fn(self, n: NestPlan) -> list[str]:
+        """Plane-marching quad kernel (see :func:`march_plan`): a thread owns
+        one aligned quad of a row and walks ``Z`` consecutive values of the
+        outermost chain index.  Because the plane stride is a multiple of the
+        quad, the chunks a reference at plane offset ``d`` needs at step
+        ``s + 1`` are the ones the reference at ``d + 1`` loaded at step
+        ``s``: they move between registers and only the leading plane is
+        loaded (NAS-MG resid: 9 of 25 chunks per step).  No shared memory, no
+        barrier; coalescing is the quad kernel's (adjacent lanes, adjacent
+        quads).  Lanes evaluate the same C expression tree (bit-exact)."""
+        prog = self.prog
+        lid = n.root
+        qp = n.quad
+        mp = qp["march"]
+        Z = mp["Z"]
+        D = len(n.chain)
+        iv = [prog.loops[c].index_var for c in n.chain]
+        kv = iv[-1]
+        minb = self.spec.get("flat_min_blocks")
+        bt = int(self.spec.get("march_block", MARCH_BLOCK))
+        lb = f"{bt}, {int(minb)}" if minb else f"{bt}"
+        out = [f'extern "C" __global__ void __launch_bounds__({lb}) {n.kernel}(const KA_L{lid} a) {{']
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        out.extend(self._locals(n, "  "))
+        out.append("  const uint32_t stride = gridDim.x * blockDim.x;")
+        out.append("  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {")
+        out.append("    if (t == a.total - 1u) {")
+        out.extend(self._finals(n, "      "))
+        out.append("    }")
+        out.append("    uint32_t r = t;")
+        for d in range(D - 1, 0, -1):
+            nm = "q_" if d == D - 1 else f"v{iv[d]}_"
+            out.append(f"    uint32_t {nm};")
+            out.append(f"    {{ uint32_t q = b2o_fastdiv(r, a.mul[{d}], a.shr[{d}]); {nm} = r - q * a.tn[{d}]; r = q; }}")
+        out.append(f"    const uint32_t z0_ = r * {Z}u;")
+        out.append(f"    const uint32_t zn_ = min({Z}u, a.n[0] - z0_);")
+        for d in range(1, D - 1):
+            out.append(f"    const int32_t v{iv[d]} = a.lo[{d}] + (int32_t)v{iv[d]}_;")
+        out.append(f"    int32_t v{iv[0]} = a.lo[0] + (int32_t)z0_;")
+        row = [f"(int64_t){c} * v{v}" for v, c in zip(qp["ovars"], qp["outer"]) if c]
+        out.append(f"    const int64_t F0_ = {' + '.join(row) if row else '0'};")
+        out.append(f"    int64_t b_ = ((F0_ + a.lo[{D - 1}]) & ~(int64_t){QUAD - 1}) + (int64_t){QUAD} * q_;")
+        out.append(f"    const int32_t k0_ = (int32_t)(b_ - F0_);")
+        out.append(f"    const int32_t kr_ = k0_ - a.lo[{D - 1}];")
+        out.append(f"    const int32_t kn_ = (int32_t)a.n[{D - 1}];")
+        out.append(f"    if (kr_ + {QUAD - 1} < 0 || kr_ >= kn_) continue;")
+        C0 = mp["C0"]
+        keys = mp["keys"]  # {(v, d, o)} chunks relative to the current plane
+
+        def cname(v, d, o):
+            return f"h{v}_{'m' if d < 0 else ''}{abs(d)}_{'m' if o < 0 else ''}{abs(o)}"
+
+        def ldexpr(v, d, o, ahead=0):
+            vt = "float4" if self.T(v) == "float" else "int4"
+            off = (d + ahead) * C0 // QUAD + o
+            if v in qp["writes"]:
+                return f"(reinterpret_cast<const {vt} *>(v{v} + b_)[{off}])"
+            return f"__ldg(reinterpret_cast<const {vt} *>(v{v} + b_) + ({off}))"
+
+        for v, d, o in sorted(keys):
+            vt = "float4" if self.T(v) == "float" else "int4"
+            out.append(f"    {vt} {cname(v, d, o)} = {ldexpr(v, d, o)};")
+        carried = {k for k in keys if (k[0], k[1] + 1, k[2]) in keys and k[0] not in qp["writes"]}
+        lead = sorted(keys - carried)
+        # software pipelining: the chunks the next plane loads are issued
+        # before this plane's arithmetic (prefetch registers n*)
+        pipe = bool(self.spec.get("march_prefetch", False))  # measured slower
+        if pipe:
+            for v, d, o in lead:
+                vt = "float4" if self.T(v) == "float" else "int4"
+                out.append(f"    {vt} n{cname(v, d, o)};")
+        out.append("    for (uint32_t s_ = 0; s_ < zn_; ++s_) {")
+        out.append("      if (s_ > 0) {")
+        out.append(f"        b_ += (int64_t){C0}; ++v{iv[0]};")
+        # ascending plane offset: the old value of (d+1) is read before it
+        # is replaced
+        for v, d, o in sorted(keys, key=lambda k: (k[1], k[0], k[2])):
+            if (v, d, o) in carried:
+                out.append(f"        {cname(v, d, o)} = {cname(v, d + 1, o)};")
+            elif pipe:
+                out.append(f"        {cname(v, d, o)} = n{cname(v, d, o)};")
+            else:
+                out.append(f"        {cname(v, d, o)} = {ldexpr(v, d, o)};")
+        out.append("      }")
+        if pipe:
+            out.append("      if (s_ + 1 < zn_) {")
+            for v, d, o in lead:
+                out.append(f"        n{cname(v, d, o)} = {ldexpr(v, d, o, 1)};")
+            out.append("      }")
+        ivs = set(qp["ivs"])
+        latest: dict[int, int] = {}
+
+        def lane_expr(e, u):
+            k = e[0]
+            if k == "arr" and e[1] in latest:
+                return f"r{latest[e[1]]}_{u}"
+            if k == "arr":
+                c = affine(e[2], ivs)[1]
+                d, rest = mp["split"](c)
+                el = rest + u
+                return f"{cname(e[1], d, el // QUAD)}.{'xyzw'[el % QUAD]}"
+            if k == "var" and e[1] == kv:
+                return f"(k0_ + {u})"
+            if k in ("num", "var"):
+                return render(e, self.local_name)
+            return f"({lane_expr(e[2], u)} {e[1]} {lane_expr(e[3], u)})"
+
+        body = prog.regions[prog.loops[n.chain[-1]].body].statements
+        for si, st in enumerate(body):
+            v = st.target[1]
+            T = self.T(v)
+            for u in range(QUAD):
+                out.append(f"      const {T} r{si}_{u} = ({T})({lane_expr(st.value, u)});")
+            latest[v] = si
+        for si, st in enumerate(body):
+            v = st.target[1]
+            c = qp["writes"][v]
+            lanes = [f"r{si}_{u}" for u in range(QUAD)]
+            masked = [f"        if ((uint32_t)(kr_ + {u}) < (uint32_t)kn_) v{v}[b_ + ({c + u})] = r{si}_{u};"
+                      for u in range(QUAD)]
+            if c % QUAD == 0:
+                vt = "float4" if self.T(v) == "float" else "int4"
+                mk = "make_float4" if vt == "float4" else "make_int4"
+                out.append(f"      if (kr_ >= 0 && kr_ + {QUAD} <= kn_) {{")
+                out.append(f"        reinterpret_cast<{vt} *>(v{v} + b_)[{c // QUAD}] = {mk}({', '.join(lanes)});")
+                out.append("      } else {")
+                out.extend(masked)
+                out.append("      }")
+            else:
+                out.append("      {")
+                out.extend(masked)
+                out.append("      }")
+        out.append("    }")
         for v in n.locals_:
             out.append(f"    (void)v{v};")
         out.append("  }")
@@ -1364,7 +1642,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "reductions")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:
