@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-21"
+COMPILER_VERSION = "b2o-compiler-23"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -160,6 +160,7 @@ class NestPlan:
     staged: dict = None     # stencil kernels: var -> {ci, cj, dmin, planes}
     streams: dict = None    # stencil kernels: var -> {ci, base}: one affine read per point
     quad: dict = None       # quad kernels: quad_plan() result
+    ktile: dict = None      # k-reduction tiled kernels: ktile_plan() result
     reds: dict = None       # reduction scalars of a chained nest: var -> "+" | "-" (reductions.py)
 
 
@@ -384,6 +385,94 @@ def march_plan(prog: Program, chain: list[int], qp: dict, Z: int) -> dict | None
     return {"Z": Z, "C0": C0, "keys": keys, "split": split}
 
 
+KT_TI = KT_TJ = 64   # k-reduction tiles: points per CTA along the two chain loops
+KT_BK = 32           # k per shared-memory stage
+KT_R = 4             # register micro-tile: KT_R x KT_R points per thread (256 threads)
+
+
+def ktile_plan(prog: Program, chain: list[int], precision: str) -> dict | None:
+    """Register-tiled k-reduction eligibility (the naive matmul nest and its
+    relatives): two parallel chain loops (i, j) whose body is straight-line
+    array assignments around exactly one sequential loop k, where
+
+    * every array written in the body is indexed by one affine form of
+      (i, j) only (a per-point accumulator, held in a register), and read
+      only at that index;
+    * inside the k loop every other array reference is affine in (i, k)
+      only ("A" operands) or (k, j) only ("B" operands) and the array is not
+      written by the nest: these are staged through shared memory tiles;
+    * the k loop's bounds use literals and read-only scalars only.
+
+    Each point still executes its statements in the original order (k
+    ascending, same C expression per statement), so results are
+    bit-identical to the sequential loop.  Returns the plan or None."""
+    if len(chain) != 2 or precision != "fp32":
+        return None
+    iv, jv = (prog.loops[c].index_var for c in chain)
+    body = prog.regions[prog.loops[chain[1]].body].statements
+    if any(st.kind not in ("assign", "loop") for st in body):
+        return None
+    kls = [x for x, st in enumerate(body) if st.kind == "loop"]
+    if len(kls) != 1:
+        return None
+    K = prog.loops[body[kls[0]].loop]
+    kv = K.index_var
+    kbody = prog.regions[K.body].statements
+    if not kbody or any(st.kind != "assign" for st in kbody):
+        return None
+    for b in (K.lower, K.upper):
+        if any(prog.vars[v].is_array or v in (iv, jv, kv) for v in expr_vars(b)):
+            return None
+    outer = body[:kls[0]] + body[kls[0] + 1:]
+    accs: dict = {}
+    for st in outer + kbody:
+        t = st.target
+        if t[0] != "arr" or ctype(prog, t[1], precision) != "float":
+            return None
+        aff = affine(t[2], {iv, jv})
+        if aff is None:
+            return None
+        key = (tuple(sorted(aff[0].items())), aff[1])
+        if accs.setdefault(t[1], key) != key:
+            return None
+    direct, tiles = set(), {}
+    for inner, sts in ((False, outer), (True, kbody)):
+        for st in sts:
+            refs: list = []
+            _array_refs(st.value, refs)
+            _array_refs(st.target[2], refs)
+            for r in refs:
+                v = r[1]
+                if v in accs:
+                    aff = affine(r[2], {iv, jv})
+                    if aff is None or (tuple(sorted(aff[0].items())), aff[1]) != accs[v]:
+                        return None
+                    continue
+                if ctype(prog, v, precision) != "float":
+                    return None
+                if not inner:
+                    if affine(r[2], {iv, jv}) is None:
+                        return None
+                    direct.add(v)
+                    continue
+                aff = affine(r[2], {iv, jv, kv})
+                if aff is None:
+                    return None
+                co = aff[0]
+                if co.get(jv, 0) == 0:
+                    side = "A"
+                elif co.get(iv, 0) == 0:
+                    side = "B"
+                else:
+                    return None
+                key = (v, tuple(sorted(co.items())), aff[1])
+                tiles.setdefault(key, (side, len(tiles)))
+    if not tiles:
+        return None
+    return {"iv": iv, "jv": jv, "kv": kv, "kloop": K.id, "kpos": kls[0], "accs": accs, "tiles": tiles,
+            "direct": direct}
+
+
 def _first_access_is_read(prog: Program, lid: int, vid: int) -> bool:
     """Walk the nest in execution order of one thread's first iteration; True
     when ``vid`` may be read before any write (conservative)."""
@@ -515,6 +604,12 @@ class _Gen:
                         if qp["groups"] == 1 and not spec.get("quad_shfl"):
                             qp["march"] = march_plan(prog, nst.chain, qp, int(spec.get("quad_march", MARCH_Z)))
                         nst.shape, nst.quad, nst.ppt = "quad", qp, 1
+        if spec.get("ktile", True):
+            for nst in self.nests.values():
+                if nst.shape == "flat" and len(nst.chain) == 2 and not nst.reds:
+                    kp = ktile_plan(prog, nst.chain, self.precision)
+                    if kp is not None:
+                        nst.shape, nst.ktile, nst.ppt = "ktile", kp, 1
         self.device_op = {}
         for l in prog.loops:
             self.device_op[l.id] = any(st.kind == "replaced" for st in prog.walk(l.body))
@@ -764,7 +859,10 @@ class _Gen:
             out.append(f"  a.p{v} = ({const}{self.T(v)} *)ex->dev[{v}];")
         for v in n.scalar_args:
             out.append(f"  a.s{v} = S{v};")
-        if n.shape == "brick":
+        if n.shape == "ktile":
+            out.append(f"  geom[0] = (a.n[1] + {KT_TJ - 1}) / {KT_TJ}; geom[1] = (a.n[0] + {KT_TI - 1}) / {KT_TI}; "
+                       f"geom[2] = 1; geom[3] = {KT_TI * KT_TJ // (KT_R * KT_R)}; geom[4] = geom[5] = 1;")
+        elif n.shape == "brick":
             tk, tj = STENCIL_TILE
             out.append(f"  geom[0] = (a.n[2] + {tk - 1}) / {tk}; geom[1] = (a.n[1] + {tj - 1}) / {tj}; "
                        f"geom[2] = (a.n[0] + {BRICK_DEPTH - 1}) / {BRICK_DEPTH}; geom[3] = {tk}; geom[4] = {tj}; "
@@ -820,6 +918,8 @@ class _Gen:
             return self.stencil_kernel_fn(n)
         if n.shape == "brick":
             return self.brick_kernel_fn(n)
+        if n.shape == "ktile":
+            return self.ktile_kernel_fn(n)
         if n.shape == "quad" and n.quad.get("march"):
             return self.quad_march_kernel_fn(n)
         if n.shape == "quad":
@@ -1276,6 +1376,189 @@ class _Gen:
         out.append("}")
         return out
 
+    def ktile_kernel_fn(self, n: NestPlan) -> list[str]:
+        """Register-tiled k-reduction kernel (see :func:`ktile_plan`): a CTA
+        of 256 threads owns a 64 x 64 block of (i, j) points, each thread a
+        4 x 4 micro-tile whose accumulators live in registers.  The k loop
+        runs in stages of 32: the A operands (i, k) and B operands (k, j) of
+        the stage are staged in shared memory (coalesced along whichever index
+        has unit stride), then every point applies the k-loop statements for
+        k ascending, each statement the same C expression as the CPU path, so
+        the per-point operation sequence (and every rounding) is the
+        sequential loop's."""
+        prog = self.prog
+        lid = n.root
+        kp = n.ktile
+        iv, jv, kv = kp["iv"], kp["jv"], kp["kv"]
+        R, TI, TJ, BK = KT_R, KT_TI, KT_TJ, KT_BK
+        nthr = TI * TJ // (R * R)
+        TX = TJ // R  # threads along j
+        K = prog.loops[kp["kloop"]]
+        body = prog.regions[prog.loops[n.chain[1]].body].statements
+        kbody = prog.regions[K.body].statements
+        pre, post = body[:kp["kpos"]], body[kp["kpos"] + 1:]
+        out = [f'extern "C" __global__ void __launch_bounds__({nthr}) {n.kernel}(const KA_L{lid} a) {{']
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        out.extend(self._locals(n, "  "))
+        tiles = sorted(kp["tiles"].items(), key=lambda x: x[1][1])
+        for (v, co, c0), (side, t) in tiles:
+            ext = TI if side == "A" else TJ
+            out.append(f"  __shared__ __align__(16) float s{t}_[{BK}][{ext + 4}];")
+        out.append(f"  const int tx_ = threadIdx.x % {TX}, ty_ = threadIdx.x / {TX};")
+        out.append(f"  const int32_t i0_ = a.lo[0] + (int32_t)(blockIdx.y * {TI}u), "
+                   f"j0_ = a.lo[1] + (int32_t)(blockIdx.x * {TJ}u);")
+        out.append(f"  const int32_t ie_ = a.lo[0] + (int32_t)a.n[0], je_ = a.lo[1] + (int32_t)a.n[1];")
+        for p_ in range(R):
+            out.append(f"  const int32_t vI{p_} = i0_ + ty_ * {R} + {p_};")
+            out.append(f"  const int32_t vJ{p_} = j0_ + tx_ * {R} + {p_};")
+        out.append(f"  const int32_t klo_ = {self.bound(K.lower, self.local_name)}, "
+                   f"khi_ = {self.bound(K.upper, self.local_name)};")
+
+        def sub(e, p_, q_, inner):
+            """C text of ``e`` for point (p_, q_) of the micro-tile."""
+            k = e[0]
+            if k == "num":
+                return render(e, self.local_name)
+            if k == "var":
+                if e[1] == iv:
+                    return f"vI{p_}"
+                if e[1] == jv:
+                    return f"vJ{q_}"
+                if e[1] == kv:
+                    return "vK_"
+                return self.local_name(e[1], False)
+            if k == "arr":
+                v = e[1]
+                if v in kp["accs"]:
+                    return f"acc{v}_{p_}{q_}"
+                if inner:
+                    aff = affine(e[2], {iv, jv, kv})
+                    key = (v, tuple(sorted(aff[0].items())), aff[1])
+                    side, t = kp["tiles"][key]
+                    return f"a{t}_{p_}" if side == "A" else f"b{t}_{q_}"
+                return f"v{v}[{sub(e[2], p_, q_, inner)}]"
+            return f"({sub(e[2], p_, q_, inner)} {e[1]} {sub(e[3], p_, q_, inner)})"
+
+        first_read = {}
+        for st in pre + kbody + post:
+            refs: list = []
+            _array_refs(st.value, refs)
+            for r in refs:
+                if r[1] in kp["accs"]:
+                    first_read.setdefault(r[1], True)
+            first_read.setdefault(st.target[1], False)
+        for v in sorted(kp["accs"]):
+            for p_ in range(R):
+                for q_ in range(R):
+                    if first_read.get(v):
+                        idx = sub(("arr", v, self._acc_index(kp, v)), p_, q_, False)
+                        out.append(f"  float acc{v}_{p_}{q_} = (vI{p_} < ie_ && vJ{q_} < je_) ? {idx} : 0.f;")
+                    else:
+                        out.append(f"  float acc{v}_{p_}{q_} = 0.f;")
+
+        def emit(sts, inner, ind):
+            for st in sts:
+                v = st.target[1]
+                for p_ in range(R):
+                    for q_ in range(R):
+                        val = sub(st.value, p_, q_, inner)
+                        line = f"acc{v}_{p_}{q_} = (float)({val});"
+                        if inner:
+                            out.append(f"{ind}{line}")
+                        else:
+                            out.append(f"{ind}if (vI{p_} < ie_ && vJ{q_} < je_) {line}")
+
+        emit(pre, False, "  ")
+        # operand staging: each thread moves ELT elements of every tile per
+        # stage; the next stage's elements are loaded into registers while
+        # the current stage is consumed from shared memory
+        ELT = BK * max(TI, TJ) // nthr
+
+        def tile_load(side, t, v, co, c0, kb, dst, ind):
+            cod = dict(co)
+            ext = TI if side == "A" else TJ
+            ov = iv if side == "A" else jv
+            o0, oe = ("i0_", "ie_") if side == "A" else ("j0_", "je_")
+            kfast = abs(cod.get(kv, 0)) == 1 and abs(cod.get(ov, 0)) != 1
+            for r_ in range(BK * ext // nthr):
+                e = f"(threadIdx.x + {r_ * nthr})"
+                kk, oo = (f"({e} % {BK})", f"({e} / {BK})") if kfast else (f"({e} / {ext})", f"({e} % {ext})")
+                terms = [f"(int64_t){cod.get(kv, 0)} * ({kb} + {kk})", f"(int64_t){cod.get(ov, 0)} * ({o0} + {oo})"]
+                for x, c in cod.items():
+                    if x not in (kv, ov):
+                        terms.append(f"(int64_t){c} * {self.local_name(x, False)}")
+                addr = " + ".join(terms + [f"(int64_t){c0}"])
+                out.append(f"{ind}{dst(r_, kk, oo)} = ({kb} + {kk} < khi_ && {o0} + {oo} < {oe}) "
+                           f"? __ldg(v{v} + ({addr})) : 0.f;")
+
+        def tile_store(side, t, v, co, c0, ind):
+            cod = dict(co)
+            ext = TI if side == "A" else TJ
+            ov = iv if side == "A" else jv
+            kfast = abs(cod.get(kv, 0)) == 1 and abs(cod.get(ov, 0)) != 1
+            for r_ in range(BK * ext // nthr):
+                e = f"(threadIdx.x + {r_ * nthr})"
+                kk, oo = (f"({e} % {BK})", f"({e} / {BK})") if kfast else (f"({e} / {ext})", f"({e} % {ext})")
+                out.append(f"{ind}s{t}_[{kk}][{oo}] = p{t}_{r_};")
+
+        for (v, co, c0), (side, t) in tiles:
+            ext = TI if side == "A" else TJ
+            for r_ in range(BK * ext // nthr):
+                out.append(f"  float p{t}_{r_};")
+        for (v, co, c0), (side, t) in tiles:
+            tile_load(side, t, v, co, c0, "klo_", lambda r_, kk, oo, t=t: f"p{t}_{r_}", "  ")
+        for (v, co, c0), (side, t) in tiles:
+            tile_store(side, t, v, co, c0, "  ")
+        out.append("  __syncthreads();")
+        out.append(f"  for (int32_t kb_ = klo_; kb_ < khi_; kb_ += {BK}) {{")
+        out.append(f"    const int32_t kn_ = min({BK}, khi_ - kb_);")
+        out.append(f"    if (kb_ + {BK} < khi_) {{")
+        for (v, co, c0), (side, t) in tiles:
+            tile_load(side, t, v, co, c0, f"(kb_ + {BK})", lambda r_, kk, oo, t=t: f"p{t}_{r_}", "      ")
+        out.append("    }")
+        out.append("#pragma unroll 4")
+        out.append("    for (int kk_ = 0; kk_ < kn_; ++kk_) {")
+        out.append("      const int32_t vK_ = kb_ + kk_;")
+        for (v, co, c0), (side, t) in tiles:
+            nm, off = (f"a{t}", "ty_") if side == "A" else (f"b{t}", "tx_")
+            out.append(f"      const float4 {nm}q_ = *reinterpret_cast<const float4 *>(&s{t}_[kk_][{off} * {R}]);")
+            for p_ in range(R):
+                out.append(f"      const float {nm}_{p_} = {nm}q_.{'xyzw'[p_]};")
+        emit(kbody, True, "      ")
+        out.append("      (void)vK_;")
+        out.append("    }")
+        out.append(f"    if (kb_ + {BK} < khi_) {{")
+        out.append("      __syncthreads();")
+        for (v, co, c0), (side, t) in tiles:
+            tile_store(side, t, v, co, c0, "      ")
+        out.append("      __syncthreads();")
+        out.append("    }")
+        out.append("  }")
+        emit(post, False, "  ")
+        for v in sorted(kp["accs"]):
+            for p_ in range(R):
+                for q_ in range(R):
+                    idx = sub(self._acc_index(kp, v), p_, q_, False)
+                    out.append(f"  if (vI{p_} < ie_ && vJ{q_} < je_) v{v}[{idx}] = acc{v}_{p_}{q_};")
+        out.append("  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {")
+        if kv in n.swrites:
+            out.append(f"    v{kv} = khi_ > klo_ ? khi_ : klo_;")
+        out.extend(self._finals(n, "    "))
+        out.append("  }")
+        for v in n.locals_:
+            out.append(f"  (void)v{v};")
+        out.append("}")
+        return out
+
+    def _acc_index(self, kp: dict, v: int):
+        """The index expression an accumulator array is written at."""
+        for st in self.prog.walk(self.prog.loops[self.prog.loops[kp["kloop"]].parent].body):
+            if st.kind == "assign" and st.target[1] == v:
+                return st.target[2]
+        raise CompileError(f"accumulator {v} has no assignment")
+
     def brick_kernel_fn(self, n: NestPlan) -> list[str]:
         """3-D brick tiling: the CTA stages a (BI+2) x (TJ+2) x (TK+2) box of
         each staged array (tile + one-point halo) in shared memory with ONE
@@ -1642,7 +1925,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "reductions")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:
