@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-23"
+COMPILER_VERSION = "b2o-compiler-25"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -666,6 +666,65 @@ class _Gen:
                 need.add(v)
         return need, writes
 
+    def progressive(self, lid: int) -> dict:
+        """Arrays a CPU fast loop may start reading before their download has
+        finished: read-only in the loop, every reference affine in the loop
+        indices with one non-negative coefficient ``C`` on the outermost
+        index ``x`` and literal bounds on every inner loop.  Iteration ``x``
+        then touches elements below ``C * x + K + 1`` only, so the generated
+        loop waits for that prefix of the (chunked, asynchronous) D2H copy
+        before each outer iteration.  Returns ``{array: (C, K)}``."""
+        if self.spec.get("progressive_d2h") is False:
+            return {}
+        prog = self.prog
+        if any(st.kind in ("call", "replaced") for st in prog.walk(prog.loops[lid].body)):
+            return {}
+        reads, writes = self.subtree_access(lid)
+        x = prog.loops[lid].index_var
+        rng = {}
+        for l in prog.subtree_loops(lid):
+            if l == lid:
+                continue
+            lo, hi = prog.loops[l].lower, prog.loops[l].upper
+            if lo[0] != "num" or hi[0] != "num" or lo[2] or hi[2]:
+                return {}
+            rng[prog.loops[l].index_var] = (int(lo[1]), int(hi[1]))
+        lvars = set(rng) | {x}
+        refs: dict = {}
+        for st in prog.walk(prog.loops[lid].body):
+            if st.kind == "assign":
+                rs: list = []
+                _array_refs(st.value, rs)
+                _array_refs(st.target[2], rs) if st.target[0] == "arr" else None
+                if st.target[0] == "arr":
+                    rs.append(st.target)
+                for r in rs:
+                    refs.setdefault(r[1], []).append(r[2])
+            elif st.kind == "decl" and st.init is not None:
+                rs = []
+                _array_refs(st.init, rs)
+                for r in rs:
+                    refs.setdefault(r[1], []).append(r[2])
+        out = {}
+        for v, idxs in refs.items():
+            if v in writes or not prog.vars[v].is_array:
+                continue
+            C, K = None, None
+            for e in idxs:
+                aff = affine(e, lvars)
+                if aff is None:
+                    break
+                c = aff[0].get(x, 0)
+                if c < 0 or (C is not None and c != C):
+                    break
+                C = c
+                k = aff[1] + sum(max(cv * rng[u][0], cv * rng[u][1]) for u, cv in aff[0].items() if u != x)
+                K = k if K is None else max(K, k)
+            else:
+                if C:  # C == 0: the first outer iteration needs the whole array anyway
+                    out[v] = (C, K)
+        return out
+
     @staticmethod
     def host_name(vid: int, is_array: bool) -> str:
         return f"A{vid}" if is_array else f"S{vid}"
@@ -695,7 +754,7 @@ class _Gen:
             else:
                 out.append(f"  {t} v{v} = *({t} *)ex->host[{v}];")
         body: list[str] = []
-        self.fast_loop(lid, 1, body, outer=True)
+        self.fast_loop(lid, 1, body, outer=True, waits=self.progressive(lid))
         out.extend(body)
         out.append(f" out_L{lid}:")
         for v in used:
@@ -707,7 +766,8 @@ class _Gen:
         out.append("}")
         return out
 
-    def fast_loop(self, lid: int, ind: int, out: list[str], outer: bool = False, label: int | None = None) -> None:
+    def fast_loop(self, lid: int, ind: int, out: list[str], outer: bool = False, label: int | None = None,
+                  waits: dict | None = None) -> None:
         prog = self.prog
         loop = prog.loops[lid]
         label = lid if label is None else label
@@ -716,6 +776,8 @@ class _Gen:
                    f"{render(loop.upper, self.local_name)}; {iv}++) {{")
         if prog.children(lid):
             out.append("  " * (ind + 1) + f"if (__builtin_expect(ex->stop, 0)) goto out_L{label};")
+        for v, (C, K) in sorted((waits or {}).items()):
+            out.append("  " * (ind + 1) + f"ex->host_wait(ex, {v}, (int64_t){C} * {iv} + {K + 1});")
         self.fast_region(loop.body, ind + 1, out, label)
         out.append("  " * ind + "}")
 
@@ -776,9 +838,14 @@ class _Gen:
             branches.append((f"ex->is_root[{lid}]", [f"launch_L{lid}(ex); if (ex->stop) return;"]))
         if not self.device_op[lid]:
             sid = self.access_set(*self.fast_footprint(lid))
-            branches.append((f"!ex->dev_inside[{lid}]",
-                             [f"ex->host_access(ex, {sid}); if (ex->stop) return;",
-                              f"fast_L{lid}(ex); if (ex->stop) return;"]))
+            prog_vars = self.progressive(lid)
+            if prog_vars:
+                # these arrays may still be arriving: fast_L waits per outer iteration
+                psid = self.access_set(set(prog_vars), set())
+                acc = f"ex->host_access_fast(ex, {sid}, {psid}); if (ex->stop) return;"
+            else:
+                acc = f"ex->host_access(ex, {sid}); if (ex->stop) return;"
+            branches.append((f"!ex->dev_inside[{lid}]", [acc, f"fast_L{lid}(ex); if (ex->stop) return;"]))
         hneed = set(expr_vars(loop.lower)) | (set(expr_vars(loop.upper)) - {loop.index_var})
         hsid = self.access_set(hneed, {loop.index_var})
         iv = f"S{loop.index_var}"
@@ -1925,7 +1992,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "reductions")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "progressive_d2h", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

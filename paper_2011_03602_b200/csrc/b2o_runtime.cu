@@ -93,6 +93,14 @@ struct AppDev {
   void *slab_init = nullptr; // pinned initial slab contents
   void *scratch = nullptr;   // device scratch for reduction partials (zeroed)
   std::vector<uint8_t> hv, dv, hmod, dev_dirty, host_touched;
+  // chunked asynchronous D2H still arriving in host[v] (progressive reads)
+  struct Pending {
+    int n = 0, done = 0;
+    size_t chunk = 0;
+    std::vector<cudaEvent_t> ev;
+  };
+  std::vector<Pending> pend;
+  bool async_d2h = true;
   std::vector<uint8_t> is_root, dev_inside, hook_mask;
   std::vector<std::vector<b2o_directive>> hooks[2];
   b2o_exec ex{};
@@ -231,7 +239,54 @@ void copy_h2d(AppDev *d, int v) {
   d->acc.h2d_bytes += var_bytes(d, v);
 }
 
-void copy_d2h(AppDev *d, int v) {
+constexpr size_t kAsyncD2hMin = (size_t)4 << 20;   // arrays below this download in one piece
+constexpr size_t kAsyncD2hChunk = (size_t)1 << 20;
+constexpr int kAsyncD2hMaxChunks = 64;
+
+// block until the first `need` bytes of a pending download are in host[v]
+void wait_host(AppDev *d, int v, size_t need) {
+  AppDev::Pending &p = d->pend[v];
+  while (p.done < p.n && (size_t)p.done * p.chunk < need) {
+    cuda_ok(d, cudaEventSynchronize(p.ev[p.done]), "D2H chunk wait");
+    ++p.done;
+  }
+  if (p.done >= p.n) p.n = p.done = 0;
+}
+
+void wait_host_all(AppDev *d) {
+  for (size_t v = 0; v < d->pend.size(); ++v)
+    if (d->pend[v].n) wait_host(d, (int)v, SIZE_MAX);
+}
+
+void copy_d2h(AppDev *d, int v, bool async_ok = false) {
+  const size_t bytes = var_bytes(d, v);
+  if (VI(d, v).is_array && async_ok && d->async_d2h && bytes >= kAsyncD2hMin) {
+    // chunked download, one event per chunk: the CPU loop that reads the
+    // array starts on the first chunk while the rest is still on the link
+    wait_host(d, v, SIZE_MAX);
+    AppDev::Pending &p = d->pend[v];
+    size_t chunk = std::max(kAsyncD2hChunk, (bytes + kAsyncD2hMaxChunks - 1) / kAsyncD2hMaxChunks);
+    chunk = (chunk + 4095) & ~(size_t)4095;
+    const int n = (int)((bytes + chunk - 1) / chunk);
+    while ((int)p.ev.size() < n) {
+      cudaEvent_t e;
+      if (!cuda_ok(d, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "D2H event")) return;
+      p.ev.push_back(e);
+    }
+    for (int k = 0; k < n; ++k) {
+      const size_t off = (size_t)k * chunk, len = std::min(chunk, bytes - off);
+      cuda_ok(d, cudaMemcpyAsync((char *)d->host[v] + off, (const char *)d->dev[v] + off, len,
+                                 cudaMemcpyDeviceToHost, d->w->stream),
+              "D2H chunk copy");
+      cuda_ok(d, cudaEventRecord(p.ev[k], d->w->stream), "D2H chunk event");
+    }
+    p.n = n;
+    p.done = 0;
+    p.chunk = chunk;
+    d->acc.d2h_bytes += bytes;
+    d->host_touched[v] = 1;
+    return;
+  }
   if (VI(d, v).is_array) {
     cuda_ok(d, cudaMemcpyAsync(d->host[v], d->dev[v], var_bytes(d, v), cudaMemcpyDeviceToHost, d->w->stream),
             "D2H copy");
@@ -245,14 +300,15 @@ void copy_d2h(AppDev *d, int v) {
   d->host_touched[v] = 1;
 }
 
-// make the host copy current (coherent mode)
-void ensure_host(AppDev *d, int v) {
+// make the host copy current (coherent mode); async_ok: the caller waits
+// for the bytes it reads (progressive CPU loops)
+void ensure_host(AppDev *d, int v, bool async_ok = false) {
   if (d->hv[v]) return;
   if (d->mode == B2O_MODE_LITERAL) {
     d->acc.stale_reads++;
     return;
   }
-  copy_d2h(d, v);
+  copy_d2h(d, v, async_ok);
   d->acc.unplanned_bytes += var_bytes(d, v);
   d->hv[v] = 1;
 }
@@ -285,11 +341,22 @@ void prepare_dev_write(AppDev *d, int v, uint64_t *counter) {
 // callbacks used by generated code
 // ---------------------------------------------------------------------------
 
-void cb_host_access(b2o_exec *ex, int32_t set) {
-  AppDev *d = D(ex);
+void host_access_impl(AppDev *d, int32_t set, const b2o_varset *prog) {
+  b2o_exec *ex = &d->ex;
   const b2o_varset &all = d->app->info->sets[set];
   const b2o_varset &wr = d->app->info->set_writes[set];
-  for (int i = 0; i < all.n && !ex->stop; ++i) ensure_host(d, all.vars[i]);
+  for (int i = 0; i < all.n && !ex->stop; ++i) {
+    const int v = all.vars[i];
+    bool progressive = false;
+    for (int j = 0; prog && j < prog->n; ++j) progressive |= prog->vars[j] == v;
+    if (progressive) {
+      ensure_host(d, v, true);
+    } else {
+      wait_host(d, v, SIZE_MAX);
+      ensure_host(d, v);
+    }
+  }
+  for (int i = 0; i < wr.n; ++i) wait_host(d, wr.vars[i], SIZE_MAX);
   for (int i = 0; i < wr.n; ++i) {
     int v = wr.vars[i];
     d->hv[v] = 1;
@@ -297,6 +364,18 @@ void cb_host_access(b2o_exec *ex, int32_t set) {
     d->hmod[v] = 1;
     d->host_touched[v] = 1;
   }
+}
+
+void cb_host_access(b2o_exec *ex, int32_t set) { host_access_impl(D(ex), set, nullptr); }
+
+void cb_host_access_fast(b2o_exec *ex, int32_t set, int32_t progressive) {
+  AppDev *d = D(ex);
+  host_access_impl(d, set, &d->app->info->sets[progressive]);
+}
+
+void cb_host_wait(b2o_exec *ex, int32_t var, int64_t elems) {
+  AppDev *d = D(ex);
+  if (d->pend[var].n) wait_host(d, var, (size_t)std::max<int64_t>(elems, 0) * elem_bytes(VI(d, var).elem));
 }
 
 void cb_pre_launch(b2o_exec *ex, int32_t loop) {
@@ -360,7 +439,7 @@ void cb_hook(b2o_exec *ex, int32_t loop, int32_t side) {
       if (d->mode == B2O_MODE_COHERENT && d->hv[v]) {
         d->acc.elided_bytes += bytes;
       } else {
-        copy_d2h(d, v);
+        copy_d2h(d, v, true);  // every host reader waits for the bytes it touches
         d->acc.planned_bytes += bytes;
       }
       d->hv[v] = 1;
@@ -370,6 +449,7 @@ void cb_hook(b2o_exec *ex, int32_t loop, int32_t side) {
 
 void cb_block(b2o_exec *ex, int32_t block) {
   AppDev *d = D(ex);
+  wait_host_all(d);
   const b2o_op_info &op = d->app->info->blocks[block];
   // a library call owns its operand transfers (as cuBLAS/cuFFT on host data)
   int saved = d->mode;
@@ -411,6 +491,7 @@ void cb_block(b2o_exec *ex, int32_t block) {
 
 void cb_external(b2o_exec *ex, int32_t call) {
   AppDev *d = D(ex);
+  wait_host_all(d);
   const b2o_op_info &op = d->app->info->calls[call];
   if (op.op < 0) {
     set_error(d, B2O_RUNTIME_ERROR, "opaque call without a CPU binding");
@@ -535,6 +616,10 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
   ex.hook_mask = d->hook_mask.data();
   ex.hook = cb_hook;
   ex.host_access = cb_host_access;
+  ex.host_access_fast = cb_host_access_fast;
+  ex.host_wait = cb_host_wait;
+  d->pend.assign(nv, AppDev::Pending{});
+  d->async_d2h = getenv("B2O_SYNC_D2H") == nullptr;
   ex.pre_launch = cb_pre_launch;
   ex.launch = cb_launch;
   ex.block = cb_block;
@@ -560,6 +645,7 @@ void par_memcpy(void *dst, const void *src, size_t bytes) {
 
 // restore pristine state; host copies valid, device copies "not present"
 void reset_state(AppDev *d) {
+  wait_host_all(d);
   const b2o_module_info *info = d->app->info;
   for (int v = 0; v < info->n_vars; ++v) {
     const b2o_var_info &vi = info->vars[v];
@@ -735,6 +821,7 @@ void execute(Worker *w, Job &j) {
     auto t0 = Clock::now();
     j.app->run(&d->ex);
     cudaError_t e = cudaStreamSynchronize(w->stream);
+    wait_host_all(d);  // downloads no CPU loop waited for are complete with the stream
     auto t1 = Clock::now();
     w->running = nullptr;
     w->deadline_ns = 0;
@@ -1076,6 +1163,7 @@ int b2o_bench_replay(uint64_t app, int32_t worker, const b2o_pattern *pattern, i
   d->recording = true;
   a->run(&d->ex);
   d->recording = false;
+  if (cudaStreamSynchronize(w->stream) == cudaSuccess) wait_host_all(d);
   if (cudaStreamSynchronize(w->stream) != cudaSuccess || d->err_validity != B2O_VALID)
     return fail("recording run failed: %s", d->err.c_str());
   if (d->log.empty()) return fail("pattern launches no kernel");
