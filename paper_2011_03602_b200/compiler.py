@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-25"
+COMPILER_VERSION = "b2o-compiler-26"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -997,13 +997,17 @@ class _Gen:
         minb = self.spec.get("flat_min_blocks")
         lb = f"{BLOCK_THREADS}, {int(minb)}" if minb else f"{BLOCK_THREADS}"
         out = [f'extern "C" __global__ void __launch_bounds__({lb}) {n.kernel}(const KA_L{lid} a) {{']
-        for v in n.arrays:
-            const = "const " if v not in n.writes else ""
-            out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
         for v in (n.reds or {}):
             out.append(f"  {self.T(v)} rd{v} = ({self.T(v)})0;  // per-thread partial of reduction {prog.vars[v].name}")
         self._reds = n.reds or {}
         out.append("  auto point = [&](const uint32_t t) {")
+        # the restrict pointers are declared inside the lambda: captured by
+        # reference they lose __restrict__, and a store through one array
+        # would then order every later load (an in-thread k loop turns into
+        # one memory round trip per iteration)
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"    {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
         D = len(n.chain)
         for c in n.chain:
             out.append(f"    int32_t v{prog.loops[c].index_var}_;")
