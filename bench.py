@@ -352,7 +352,8 @@ def ga_arm(args, dist: Dist) -> dict | None:
 
     g = golden(args.ga_workload)
     model = load_ir_document(json.dumps(g["doc"]))
-    ev = B200Evaluator(g["spec"], devices=[dist.local_rank], timeout_seconds=args.ga_timeout)
+    ev = B200Evaluator(g["spec"], devices=[dist.local_rank], timeout_seconds=args.ga_timeout,
+                       dedupe=bool(args.ga_dedupe))
     ev.app_for(g["doc"])  # compile + load + all-CPU reference run, untimed
     evaluator = ShardedEvaluator(ev) if dist.world > 1 else ev
     params = GAParams(population_size=args.ga_pop, generations=args.ga_gens, seed=args.ga_seed)
@@ -364,12 +365,16 @@ def ga_arm(args, dist: Dist) -> dict | None:
     valid = sum(1 for r in ev.log if r.get("validity") == "valid")
     local = dist.sum(float(len(ev.log)))
     fit_sum = dist.sum(float(sum(r.get("time_s") or 0.0 for r in ev.log)))
+    programs = dist.sum(float(ev.programs_executed))
     return {"workload": f"{args.ga_workload} inline nn={sweeps_of(g['doc'])}, pop {args.ga_pop} x {args.ga_gens} gens",
             "patterns_per_s": round(res.evaluations_performed / wall, 3), "evaluations": res.evaluations_performed,
             "cache_hits": res.cache_hits, "wall_s": round(wall, 3), "best_genome": "".join(map(str, res.best_genome)),
             "best_time_s": res.best_time, "measured_by_all_ranks": int(local), "valid_on_rank0": valid,
             "speculated": stats.get("speculated", 0), "speculated_unused": stats.get("speculated_unused", 0),
             "sum_fitness_s_all_ranks": round(fit_sum, 3),
+            "programs_executed_all_ranks": int(programs),
+            "dedupe": ("genomes whose GPU roots and transfer plan coincide share one program run "
+                       "(B200Evaluator.run_key, SURVEY.md §8e)") if args.ga_dedupe else "off",
             "history_evals": [h.evaluations for h in res.history][:6]}
 
 
@@ -470,6 +475,7 @@ def main() -> None:
     ap.add_argument("--ga-gens", type=int, default=20)
     ap.add_argument("--ga-seed", type=int, default=20201106)
     ap.add_argument("--ga-timeout", type=float, default=120.0)
+    ap.add_argument("--ga-dedupe", type=int, default=1, help="run identical programs (same GPU roots + plan) once")
     args = ap.parse_args()
     dist = Dist()
     try:

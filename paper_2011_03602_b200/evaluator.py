@@ -106,7 +106,7 @@ class B200Evaluator:
 
     def __init__(self, app_spec: dict, devices: list[int] | None = None, mode: str = "coherent",
                  timeout_seconds: float = 300.0, repeats: int = 1, reference_outputs: dict | None = None,
-                 cache_dir=None):
+                 cache_dir=None, dedupe: bool = True):
         if mode not in ("coherent", "literal"):
             raise ValueError(f"unknown mode {mode!r}")
         self.spec = dict(app_spec)
@@ -121,6 +121,14 @@ class B200Evaluator:
         self._docs: dict[int, tuple[object, dict]] = {}
         self._keys: dict[int, tuple[dict, str]] = {}
         self.log: list[dict] = []
+        # program-level dedupe: genomes whose GPU roots and
+        # transfer plan coincide run the identical program, so it is executed
+        # once and its measurement shared (reported: programs_executed vs
+        # dedupe_hits; dedupe=False measures every request)
+        self.dedupe = dedupe
+        self._runs: dict = {}
+        self.programs_executed = 0
+        self.dedupe_hits = 0
 
     @property
     def parallel_width(self) -> int:
@@ -211,23 +219,45 @@ class B200Evaluator:
         except B2OError as exc:
             return [{"validity": "runtime_error", "time_s": None, "diag": str(exc)[-250:]} for _ in payloads]
 
+    @staticmethod
+    def run_key(doc_key: str, payload: dict) -> str:
+        """What the runtime executes for a payload: the program, its GPU
+        roots and every directive (the genome text and the cost-model
+        priority do not change the run)."""
+        dirs = sorted(json.dumps(d, sort_keys=True) for d in payload["directives"])
+        return json.dumps([doc_key, sorted(payload["gpu_roots"]), dirs], sort_keys=True)
+
     def measure_batch(self, requests) -> list:
         groups: dict[str, list[int]] = {}
         docs: dict[str, dict] = {}
         payloads = []
+        keys = []
         for i, req in enumerate(requests):
             doc = self._doc(req.model)
             key = document_digest(doc)
             docs[key] = doc
-            groups.setdefault(key, []).append(i)
             payloads.append(payload_from_request(req))
+            keys.append(self.run_key(key, payloads[i]))
+            if self.dedupe and (keys[i] in self._runs or keys[i] in keys[:i]):
+                continue  # the identical program is (being) measured already
+            groups.setdefault(key, []).append(i)
         out: list = [None] * len(requests)
         for key, idxs in groups.items():
             results = self.measure_payloads(docs[key], [payloads[i] for i in idxs])
+            self.programs_executed += len(idxs)
             for i, r in zip(idxs, results):
                 r = dict(r)
                 r["genome"] = payloads[i]["genome"]
+                if self.dedupe:
+                    self._runs[keys[i]] = r
                 self.log.append(r)
+                out[i] = self._result(r["validity"], r.get("time_s"), r)
+        for i in range(len(requests)):
+            if out[i] is None:
+                r = dict(self._runs[keys[i]])
+                r["dedupe_of"] = r.pop("genome")
+                r["genome"] = payloads[i]["genome"]
+                self.dedupe_hits += 1
                 out[i] = self._result(r["validity"], r.get("time_s"), r)
         return out
 

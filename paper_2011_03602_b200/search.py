@@ -239,9 +239,32 @@ class ShardedEvaluator:
     def measure(self, request):
         return self.measure_batch([request])[0]
 
+    def _run_keys(self, requests) -> list | None:
+        """Program-level dedupe keys (B200Evaluator.run_key) when the inner
+        evaluator dedupes: identical programs are measured once across ALL
+        ranks, and the results are shared through the gathered cache."""
+        if not getattr(self.inner, "dedupe", False) or not hasattr(self.inner, "run_key"):
+            return None
+        from .evaluator import payload_from_request
+        from .ir import document_digest
+
+        return [self.inner.run_key(document_digest(self.inner._doc(r.model)), payload_from_request(r))
+                for r in requests]
+
     def measure_batch(self, requests) -> list:
-        owner = lpt_assignment([_predicted_cost(r) for r in requests], self.world)
-        mine = [i for i, o in enumerate(owner) if o == self.rank]
+        keys = self._run_keys(requests)
+        if keys is None:
+            todo = list(range(len(requests)))
+        else:
+            if not hasattr(self, "_runs"):
+                self._runs: dict = {}
+            firsts: dict = {}
+            for i, k in enumerate(keys):
+                if k not in self._runs and k not in firsts:
+                    firsts[k] = i
+            todo = sorted(firsts.values())
+        owner = lpt_assignment([_predicted_cost(requests[i]) for i in todo], self.world)
+        mine = [i for i, o in zip(todo, owner) if o == self.rank]
         inner_batch = getattr(self.inner, "measure_batch", None)
         reqs = [requests[i] for i in mine]
         res = inner_batch(reqs) if inner_batch else [self.inner.measure(r) for r in reqs]
@@ -253,4 +276,10 @@ class ShardedEvaluator:
         for part in gathered:
             for i, t, validity, eid, diag in part:
                 out[i] = cls(t, validity, eid, diag)
+                if keys is not None:
+                    self._runs[keys[i]] = (t, validity, eid, diag)
+        if keys is not None:
+            for i, k in enumerate(keys):
+                if out[i] is None:
+                    out[i] = cls(*self._runs[k])
         return out

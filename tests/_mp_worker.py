@@ -3,7 +3,7 @@
 import os
 
 
-def sharded_ga(rank: int, world: int, port: int, seed: int, out_dir: str) -> None:
+def sharded_ga(rank: int, world: int, port: int, seed: int, out_dir: str, dedupe: bool = False) -> None:
     import json
     import random
 
@@ -28,8 +28,25 @@ def sharded_ga(rank: int, world: int, port: int, seed: int, out_dir: str) -> Non
             self.calls += 1
             return super().measure(request)
 
+    class DedupeCounting(Counting):
+        """Counting cost model with B200Evaluator's program-level dedupe keys."""
+
+        dedupe = True
+
+        @staticmethod
+        def run_key(doc_key, payload):
+            from paper_2011_03602_b200.evaluator import B200Evaluator
+
+            return B200Evaluator.run_key(doc_key, payload)
+
+        @staticmethod
+        def _doc(model):
+            from paper_2011_03602_b200.ir import document_of
+
+            return document_of(model)
+
     model = random_model(random.Random(seed), max_depth=3)
-    inner = Counting()
+    inner = DedupeCounting() if dedupe else Counting()
     ev = ShardedEvaluator(inner)
     stats = {}
     res = run_search_batched(model, screen_model(model), ev, GAParams(population_size=10, generations=6, seed=seed),

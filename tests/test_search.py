@@ -174,3 +174,41 @@ def test_sharded_ga_over_gloo_world2(tmp_path):
     assert r0["speculated_unused"] == r1["speculated_unused"]
     assert r0["local_calls"] + r1["local_calls"] == ref.evaluations_performed + r0["speculated_unused"]
     assert r0["local_calls"] > 0 and r1["local_calls"] > 0
+
+
+def test_sharded_ga_dedupes_identical_programs(tmp_path):
+    """Program-level dedupe across ranks: genomes with the
+    same GPU roots and transfer plan run one program; the SearchResult is
+    still the reference's, and fewer programs are measured."""
+    import multiprocessing as mp
+
+    from gpuoffload.evaluators import CostModelEvaluator
+    from gpuoffload.ga import GAParams, run_search
+    from gpuoffload.screen import screen_model
+
+    from _models import random_model
+    from _mp_worker import sharded_ga
+
+    seed = 4
+    res = {}
+    for dedupe in (False, True):
+        out = tmp_path / str(dedupe)
+        out.mkdir()
+        port = _free_port()
+        ctx = mp.get_context("spawn")
+        procs = [ctx.Process(target=sharded_ga, args=(r, 2, port, seed, str(out), dedupe)) for r in range(2)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(120)
+            assert p.exitcode == 0
+        res[dedupe] = [json.loads((out / f"rank{r}.json").read_text()) for r in range(2)]
+    model = random_model(random.Random(seed), max_depth=3)
+    ref = run_search(model, screen_model(model), CostModelEvaluator(),
+                     GAParams(population_size=10, generations=6, seed=seed))
+    for r in res[True]:
+        assert tuple(r["best"]) == ref.best_genome and r["time"] == ref.best_time
+        assert r["evals"] == ref.evaluations_performed and r["hits"] == ref.cache_hits
+        assert r["history"] == res[False][0]["history"]
+    calls = {d: sum(r["local_calls"] for r in res[d]) for d in res}
+    assert calls[True] < calls[False]  # seed 4: 18 programs measured without dedupe, 15 with
