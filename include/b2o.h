@@ -30,6 +30,7 @@
 #ifndef B2O_H
 #define B2O_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -139,6 +140,18 @@ int b2o_gemm_f32_phases(const float *A, const float *B, float *C, int64_t m, int
 /* h[d[i]] += 1 for i < n on the device (values outside [0, bins) skipped);
  * elem: element type of h, 0 = int32, 1 = fp32, 2 = fp64 (b2o_module.h b2o_elem) */
 int b2o_histogram(const int32_t *d, int64_t n, void *h, int64_t bins, int elem, void *stream);
+
+/* The sequential fp32 sum s = (((s0 + x[0]) + x[1]) + ...) -- every addition
+ * rounded to fp32 in index order, the C loop `s = s + x[i]` -- computed in
+ * parallel, bit-identical to the loop (binade-segmented integer scan,
+ * csrc/b2o_xsum.cu).  x and s_out are device pointers; asynchronous on
+ * `stream`.  Used by the opt-in GPU reductions (reductions.py) so an
+ * offloaded `gosa = gosa + gs[...]` nest (reference src/screen.py:57-68
+ * rejects it) reproduces the CPU loop exactly.  _ws: caller-provided device
+ * workspace of b2o_exact_sum_workspace(n) bytes. */
+int b2o_exact_sum_f32(const float *x, int64_t n, float s0, float *s_out, void *stream);
+size_t b2o_exact_sum_workspace(int64_t n);
+int b2o_exact_sum_f32_ws(const float *x, int64_t n, float s0, float *s_out, void *workspace, void *stream);
 
 #ifdef __cplusplus
 }

@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-26"
+COMPILER_VERSION = "b2o-compiler-27"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -162,6 +162,7 @@ class NestPlan:
     quad: dict = None       # quad kernels: quad_plan() result
     ktile: dict = None      # k-reduction tiled kernels: ktile_plan() result
     reds: dict = None       # reduction scalars of a chained nest: var -> "+" | "-" (reductions.py)
+    exact: dict = None      # reductions summed exactly in loop order (b2o_xsum.cu): var -> slot
 
 
 def affine(e, idx_vars):
@@ -585,13 +586,20 @@ class _Gen:
         self.calls: dict[int, dict] = {}
         self.nests = {l.id: plan_nest(prog, l.id, spec.get("stencil", False), bool(spec.get("reductions")))
                       for l in prog.loops}
+        self.exact_slots = 0
         for nst in self.nests.values():
-            if nst.shape == "flat" and nst.chain and nst.ppt == 1 and all(
+            ex = self.exact_reductions(nst)
+            if ex:
+                nst.exact = ex
+                nst.ppt = 1
+                self.exact_slots = max(self.exact_slots, len(ex))
+        for nst in self.nests.values():
+            if nst.shape == "flat" and nst.chain and nst.ppt == 1 and not nst.exact and all(
                     st.kind == "assign" for st in prog.regions[prog.loops[nst.chain[-1]].body].statements):
                 nst.kb = int(spec.get("flat_kblock", 1))
         if spec.get("flat_ppt"):
             for nst in self.nests.values():
-                if nst.shape == "flat" and nst.chain and all(
+                if nst.shape == "flat" and nst.chain and not nst.exact and all(
                         st.kind == "assign" for st in prog.regions[prog.loops[nst.chain[-1]].body].statements):
                     nst.ppt = int(spec["flat_ppt"])
         if int(spec.get("flat_vec", QUAD)) == QUAD and not spec.get("flat_ppt") \
@@ -632,6 +640,53 @@ class _Gen:
                         raise CompileError(f"external {c.name!r} takes scalar argument {prog.vars[v].name!r}")
                 self.calls[c.id] = b
         self.ext_writes = {cid: {b["out"]} for cid, b in self.calls.items()}
+
+    def exact_reductions(self, n: NestPlan) -> dict:
+        """Reductions of a chained nest that can be summed EXACTLY in loop
+        order on the GPU (b2o_exact_sum_f32, csrc/b2o_xsum.cu): an fp32 scalar
+        updated by ``s = s + e`` / ``s = e + s`` / ``s = s - e`` with ``e`` of
+        C type float (so the C statement is one fp32 addition), exactly once
+        per point: the statement sits directly in the innermost chain loop's
+        body and is the nest's only update of ``s``.  The kernel stores the
+        per-point terms in loop order, the runtime reproduces the sequential
+        sum bit for bit.  spec ``exact_reductions: false`` keeps the
+        reassociating tree (faster, documented tolerance).  Returns
+        ``{var: slot}``."""
+        if not n.reds or not n.chain or self.spec.get("exact_reductions") is False:
+            return {}
+        prog = self.prog
+        body = prog.regions[prog.loops[n.chain[-1]].body].statements
+        out = {}
+        for v in sorted(n.reds):
+            if self.T(v) != "float":
+                continue
+            hits = [st for st in prog.walk(prog.loops[n.root].body)
+                    if st.kind == "assign" and st.target[0] == "var" and st.target[1] == v]
+            if len(hits) != 1 or hits[0] not in body:
+                continue
+            red = reductions.reduction_stmt(hits[0])
+            if red is None or etype(prog, red[2], self.precision) != "float":
+                continue
+            out[v] = len(out)
+        return out
+
+    def exact_elems(self) -> int:
+        """Largest iteration space of a nest with exact reductions when its
+        chain bounds are literals (the runtime sizes the term buffers at
+        replica setup, outside every timed run); 0: size on first use."""
+        best = 0
+        for n in self.nests.values():
+            if not n.exact:
+                continue
+            tot = 1
+            for c in n.chain:
+                lo, hi = self.prog.loops[c].lower, self.prog.loops[c].upper
+                if lo[0] != "num" or hi[0] != "num":
+                    tot = 0
+                    break
+                tot *= max(0, int(hi[1]) - int(lo[1]))
+            best = max(best, tot)
+        return best
 
     # -- helpers -----------------------------------------------------------
 
@@ -881,6 +936,8 @@ class _Gen:
             out.append(f"  {const}{self.T(v)} *p{v};")
         for v in n.scalar_args:
             out.append(f"  {self.T(v)} s{v};")
+        for v in (n.exact or {}):
+            out.append(f"  float *xb{v};  // per-point terms of reduction {self.prog.vars[v].name}, loop order")
         out.append(f"}} KA_L{n.root};")
         return out
 
@@ -949,11 +1006,15 @@ class _Gen:
                 bt = int(self.spec.get("march_block", MARCH_BLOCK))
             per = bt * n.ppt
             cap = int(self.spec.get("flat_grid_cap", 0)) or 0x7FFFFFFF
-            if n.reds:
+            if n.reds and set(n.reds) - set(n.exact or {}):
                 cap = min(cap, 2048)  # B2O_RED_MAX_BLOCKS: one partial per CTA in the scratch
             out.append(f"  {{ uint64_t g = (total + {per - 1}) / {per}; geom[0] = (uint32_t)(g > {cap}u ? "
                        f"{cap}u : g); geom[1] = geom[2] = 1; geom[3] = {bt}; geom[4] = geom[5] = 1; }}")
+        for v, slot in (n.exact or {}).items():
+            out.append(f"  a.xb{v} = (float *)ex->red_buf(ex, {slot}, (int64_t)total); if (ex->stop) return;")
         out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, geom);")
+        for v, slot in (n.exact or {}).items():
+            out.append(f"  if (!ex->stop) ex->red_exact(ex, {v}, {slot}, (int64_t)total, a.s{v});")
         out.append("}")
         return out
 
@@ -997,9 +1058,11 @@ class _Gen:
         minb = self.spec.get("flat_min_blocks")
         lb = f"{BLOCK_THREADS}, {int(minb)}" if minb else f"{BLOCK_THREADS}"
         out = [f'extern "C" __global__ void __launch_bounds__({lb}) {n.kernel}(const KA_L{lid} a) {{']
-        for v in (n.reds or {}):
+        tree = {v: o for v, o in (n.reds or {}).items() if v not in (n.exact or {})}
+        for v in tree:
             out.append(f"  {self.T(v)} rd{v} = ({self.T(v)})0;  // per-thread partial of reduction {prog.vars[v].name}")
         self._reds = n.reds or {}
+        self._exact = n.exact or {}
         out.append("  auto point = [&](const uint32_t t) {")
         # the restrict pointers are declared inside the lambda: captured by
         # reference they lose __restrict__, and a store through one array
@@ -1077,12 +1140,13 @@ class _Gen:
             out.append("    point(t0);")
         out.append("  }")
         self._reds = {}
-        if n.reds:
-            out.extend(self._reduction_epilogue(n))
+        self._exact = {}
+        if tree:
+            out.extend(self._reduction_epilogue(n, tree))
         out.append("}")
         return out
 
-    def _reduction_epilogue(self, n: NestPlan) -> list[str]:
+    def _reduction_epilogue(self, n: NestPlan, reds: dict) -> list[str]:
         """Deterministic grid reduction: block totals (warp xor-butterfly +
         shared memory, b2o_block_sum) go to the scratch, one slot per CTA; the
         last CTA to finish (atomic ticket) sums the slots in CTA order, adds
@@ -1090,7 +1154,7 @@ class _Gen:
         grid => bit-reproducible run to run."""
         out = ["  {", "    __shared__ double b2o_red_sm[32];", "    __shared__ int b2o_last;",
                "    char *scr_ = (char *)a.scratch;", "    unsigned *cnt_ = (unsigned *)scr_;"]
-        for r, v in enumerate(n.reds):
+        for r, v in enumerate(reds):
             T = self.T(v)
             out.append(f"    {{ {T} bt = b2o_block_sum<{T}>(rd{v}, ({T} *)b2o_red_sm);")
             out.append(f"      if (threadIdx.x == 0) (({T} *)(scr_ + 256 + {r} * 8 * B2O_RED_MAX_BLOCKS))[blockIdx.x] = bt; }}")
@@ -1098,7 +1162,7 @@ class _Gen:
         out.append("    __syncthreads();")
         out.append("    if (b2o_last) {")
         out.append("      __threadfence();")
-        for r, v in enumerate(n.reds):
+        for r, v in enumerate(reds):
             T = self.T(v)
             out.append(f"      {{ const {T} *part = (const {T} *)(scr_ + 256 + {r} * 8 * B2O_RED_MAX_BLOCKS);")
             out.append(f"        {T} s = ({T})0;")
@@ -1847,7 +1911,12 @@ class _Gen:
                     out.append(pad + f"v{st.var} = {render(st.init, self.local_name)};")
             elif st.kind == "assign":
                 red = reductions.reduction_stmt(st) if getattr(self, "_reds", None) else None
-                if red is not None and red[0] in self._reds:
+                if red is not None and red[0] in getattr(self, "_exact", {}):
+                    # the term of this point, in loop order (t); s - e == s + (-e) exactly
+                    v, op, e = red
+                    sign = "-" if op == "-" else ""
+                    out.append(pad + f"a.xb{v}[t] = {sign}(float)({self.dev_expr(e)});")
+                elif red is not None and red[0] in self._reds:
                     v, op, e = red
                     out.append(pad + f"rd{v} = rd{v} {op} ({self.dev_expr(e)});")
                 else:
@@ -1972,7 +2041,8 @@ class _Gen:
         out.append("static const b2o_module_info INFO = {")
         out.append(f"  B2O_MODULE_ABI, {len(prog.vars)}, {len(prog.loops)}, {len(self.sets)}, {len(outputs)}, "
                    f"{len(self.blocks)}, {len(prog.calls)}, {prec},")
-        out.append(f'  VARS, LOOPS, SETS, SETW, OUTS, BLOCKS, CALLS, "{digest}"')
+        out.append(f'  VARS, LOOPS, SETS, SETW, OUTS, BLOCKS, CALLS, "{digest}",')
+        out.append(f"  {self.exact_slots}, {self.exact_elems()}")
         out.append("};")
         out.append('extern "C" const b2o_module_info *b2o_mod_info(void) { return &INFO; }')
         return out
@@ -1996,7 +2066,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "progressive_d2h", "reductions")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "progressive_d2h", "exact_reductions", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

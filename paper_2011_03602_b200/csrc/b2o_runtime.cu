@@ -92,6 +92,10 @@ struct AppDev {
   void *slab = nullptr;      // device scalar slab
   void *slab_init = nullptr; // pinned initial slab contents
   void *scratch = nullptr;   // device scratch for reduction partials (zeroed)
+  std::vector<void *> red_bufs;        // exact reductions: per-point terms, per slot
+  std::vector<int64_t> red_buf_elems;
+  void *xsum_ws = nullptr;             // exact-sum workspace (b2o_exact_sum_workspace)
+  size_t xsum_ws_bytes = 0;
   std::vector<uint8_t> hv, dv, hmod, dev_dirty, host_touched;
   // chunked asynchronous D2H still arriving in host[v] (progressive reads)
   struct Pending {
@@ -378,6 +382,47 @@ void cb_host_wait(b2o_exec *ex, int32_t var, int64_t elems) {
   if (d->pend[var].n) wait_host(d, var, (size_t)std::max<int64_t>(elems, 0) * elem_bytes(VI(d, var).elem));
 }
 
+bool red_reserve(AppDev *d, int32_t slot, int64_t n) {
+  if ((int32_t)d->red_bufs.size() <= slot) {
+    d->red_bufs.resize(slot + 1, nullptr);
+    d->red_buf_elems.resize(slot + 1, 0);
+  }
+  if (d->red_buf_elems[slot] < n) {
+    if (d->red_bufs[slot]) cudaFree(d->red_bufs[slot]);
+    d->red_bufs[slot] = nullptr;
+    d->red_buf_elems[slot] = 0;
+    if (!cuda_ok(d, cudaMalloc(&d->red_bufs[slot], sizeof(float) * (size_t)std::max<int64_t>(n, 1)),
+                 "exact reduction buffer"))
+      return false;
+    d->red_buf_elems[slot] = n;
+  }
+  const size_t ws = b2o_exact_sum_workspace(n);
+  if (d->xsum_ws_bytes < ws) {
+    if (d->xsum_ws) cudaFree(d->xsum_ws);
+    d->xsum_ws = nullptr;
+    d->xsum_ws_bytes = 0;
+    if (!cuda_ok(d, cudaMalloc(&d->xsum_ws, ws), "exact-sum workspace")) return false;
+    d->xsum_ws_bytes = ws;
+  }
+  return true;
+}
+
+void *cb_red_buf(b2o_exec *ex, int32_t slot, int64_t n) {
+  AppDev *d = D(ex);
+  return red_reserve(d, slot, n) ? d->red_bufs[slot] : nullptr;
+}
+
+void cb_red_exact(b2o_exec *ex, int32_t var, int32_t slot, int64_t n, float s0) {
+  AppDev *d = D(ex);
+  if (slot >= (int32_t)d->red_bufs.size() || !d->red_bufs[slot]) {
+    set_error(d, B2O_RUNTIME_ERROR, "exact reduction without its term buffer");
+    return;
+  }
+  if (b2o_exact_sum_f32_ws((const float *)d->red_bufs[slot], n, s0, (float *)((char *)d->slab + 8 * var),
+                           d->xsum_ws, d->w->stream) != 0)
+    cuda_ok(d, cudaGetLastError() == cudaSuccess ? cudaErrorUnknown : cudaGetLastError(), "exact in-order sum");
+}
+
 void cb_pre_launch(b2o_exec *ex, int32_t loop) {
   AppDev *d = D(ex);
   const b2o_loop_info &li = d->app->info->loops[loop];
@@ -618,6 +663,10 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
   ex.host_access = cb_host_access;
   ex.host_access_fast = cb_host_access_fast;
   ex.host_wait = cb_host_wait;
+  ex.red_buf = cb_red_buf;
+  ex.red_exact = cb_red_exact;
+  for (int slot = 0; slot < info->exact_slots && info->exact_elems > 0; ++slot)
+    if (!red_reserve(d.get(), slot, info->exact_elems)) return fail("exact reduction buffers");
   d->pend.assign(nv, AppDev::Pending{});
   d->async_d2h = getenv("B2O_SYNC_D2H") == nullptr;
   ex.pre_launch = cb_pre_launch;
@@ -1001,6 +1050,10 @@ int b2o_shutdown(void) {
       if (d->slab_init) cudaFreeHost(d->slab_init);
       if (d->slab) cudaFree(d->slab);
       if (d->scratch) cudaFree(d->scratch);
+    for (void *p : d->red_bufs) if (p) cudaFree(p);
+    if (d->xsum_ws) cudaFree(d->xsum_ws);
+      for (void *p : d->red_bufs) if (p) cudaFree(p);
+      if (d->xsum_ws) cudaFree(d->xsum_ws);
       if (d->mod) drv.moduleUnload(d->mod);
     }
   }
@@ -1132,6 +1185,8 @@ int b2o_app_destroy(uint64_t app) {
     if (d->slab_init) cudaFreeHost(d->slab_init);
     if (d->slab) cudaFree(d->slab);
     if (d->scratch) cudaFree(d->scratch);
+    for (void *p : d->red_bufs) if (p) cudaFree(p);
+    if (d->xsum_ws) cudaFree(d->xsum_ws);
     if (d->mod) drv.moduleUnload(d->mod);
   }
   if (a->dl) dlclose(a->dl);

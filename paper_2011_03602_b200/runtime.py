@@ -109,6 +109,11 @@ def lib() -> ctypes.CDLL:
             "b2o_histogram": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                ctypes.c_void_p], ctypes.c_int),
             "b2o_gemm_impl": ([], ctypes.c_int),
+            "b2o_exact_sum_f32": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_void_p],
+                                  ctypes.c_int),
+            "b2o_exact_sum_workspace": ([ctypes.c_int64], ctypes.c_size_t),
+            "b2o_exact_sum_f32_ws": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
             "b2o_bench_replay": ([ctypes.c_uint64, ctypes.c_int32, ctypes.POINTER(Pattern), ctypes.c_int32,
                                   ctypes.c_int32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                   ctypes.c_int32, u64p], ctypes.c_int),
