@@ -332,7 +332,7 @@ def reductions_arm(args, dist: Dist) -> dict:
     return {"genome": "100100100", "validity": last["validity"], "e2e_GBps": round(bytes_per_step / e2e_s / 1e9, 3),
             "ms_per_call": round(e2e_s * 1e3, 3), "app_run_ms": round(last["time_s"] * 1e3, 3),
             "h2d_bytes": int(last["h2d_bytes"]), "d2h_bytes": int(last["d2h_bytes"]),
-            "note": "gosa tolerance 5e-2: the sequential fp32 reference sum is 2.5% off the exact sum"}
+            "note": "gosa summed on the GPU in loop order, bit-identical to the sequential CPU loop (b2o_exact_sum_f32)"}
 
 
 def ga_arm(args, dist: Dist) -> dict | None:

@@ -37,6 +37,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <map>
@@ -143,10 +145,26 @@ __global__ void __launch_bounds__(1024) xs_summ_kernel(const float *__restrict__
   const int e = elo + k;
   int P = 0, lo = kLoEmpty, hi = kHiEmpty, flag = 0;
   const int i0 = h * (XS_CHUNK / 2), i1 = min(i0 + XS_CHUNK / 2, cnt);
-  for (int i = i0; i < i1; ++i) {
-    P += units(__float_as_uint(xs[warp][i + h]), e, flag);  // |P| < 128 * 2^24: no overflow
-    lo = min(lo, P - 1);
-    hi = max(hi, P + 1);
+  if (i1 - i0 == XS_CHUNK / 2) {
+    // full half: 8 elements per step, loads first (independent of the scan)
+#pragma unroll 2
+    for (int i = i0; i < i1; i += 8) {
+      uint32_t b[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = __float_as_uint(xs[warp][i + j + h]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        P += units(b[j], e, flag);  // |P| < 128 * 2^24: no overflow
+        lo = min(lo, P - 1);
+        hi = max(hi, P + 1);
+      }
+    }
+  } else {
+    for (int i = i0; i < i1; ++i) {
+      P += units(__float_as_uint(xs[warp][i + h]), e, flag);
+      lo = min(lo, P - 1);
+      hi = max(hi, P + 1);
+    }
   }
   Summ s{P, lo, hi, flag};
   Summ t;
@@ -200,12 +218,13 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
                                                          const double *bound, float s0,
                                                          const Summ *__restrict__ chunks,
                                                          const Summ *__restrict__ supers, int64_t nchunks,
-                                                         int64_t nsupers, float *out) {
+                                                         int64_t nsupers, float *out, int stats) {
+  int n_desc = 0, n_slow = 0, n_super_ok = 0;
   constexpr int G = 32;                       // super-chunks per window
   constexpr int REC = G * XS_W;               // records per window (int4 each)
   __shared__ int4 sbuf[2][REC];
   __shared__ int4 cbuf[XS_SUPER * XS_W];
-  __shared__ float xbuf[XS_CHUNK];
+  __shared__ __align__(16) float xbuf[XS_CHUNK];
   const int lane = threadIdx.x;
   const int elo = window_lo(bound, s0);
   const int4 *sup4 = reinterpret_cast<const int4 *>(supers);
@@ -233,7 +252,11 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
     if (g + 1 < ngroups) fetch(g + 1);
     const int64_t s_end = min((g + 1) * G, nsupers);
     for (int64_t sc = g * G; sc < s_end; ++sc) {
-      if (apply(s, reinterpret_cast<const Summ *>(&sbuf[cur][(sc - g * G) * XS_W]), elo)) continue;
+      if (apply(s, reinterpret_cast<const Summ *>(&sbuf[cur][(sc - g * G) * XS_W]), elo)) {
+        ++n_super_ok;
+        continue;
+      }
+      ++n_desc;
       const int64_t c0 = sc * XS_SUPER, c1 = min(c0 + XS_SUPER, nchunks);
       __syncwarp();
 #pragma unroll
@@ -245,6 +268,7 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
       for (int64_t c = c0; c < c1; ++c) {
         if (apply(s, reinterpret_cast<const Summ *>(&cbuf[(c - c0) * XS_W]), elo)) continue;
         // element by element: the definition
+        ++n_slow;
         const int64_t base = c * XS_CHUNK;
         const int cnt = (int)min((int64_t)XS_CHUNK, n - base);
 #pragma unroll
@@ -253,8 +277,16 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
           xbuf[i] = i < cnt ? x[base + i] : 0.f;
         }
         __syncwarp();
-        if (lane == 0)
-          for (int i = 0; i < cnt; ++i) s = __fadd_rn(s, xbuf[i]);
+        if (lane == 0) {
+          int i = 0;
+          for (; i + 8 <= cnt; i += 8) {  // operands fetched ahead of the dependent adds
+            const float4 a = *reinterpret_cast<const float4 *>(&xbuf[i]);
+            const float4 b = *reinterpret_cast<const float4 *>(&xbuf[i + 4]);
+            s = __fadd_rn(s, a.x); s = __fadd_rn(s, a.y); s = __fadd_rn(s, a.z); s = __fadd_rn(s, a.w);
+            s = __fadd_rn(s, b.x); s = __fadd_rn(s, b.y); s = __fadd_rn(s, b.z); s = __fadd_rn(s, b.w);
+          }
+          for (; i < cnt; ++i) s = __fadd_rn(s, xbuf[i]);
+        }
         s = __shfl_sync(0xffffffffu, s, 0);
         __syncwarp();
       }
@@ -264,6 +296,9 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
     __syncwarp();
   }
   if (lane == 0) *out = s;
+  if (stats && lane == 0)
+    printf("[xsum] n=%lld supers=%lld ok=%d descents=%d slow_chunks=%d elo=%d\n", (long long)n,
+           (long long)nsupers, n_super_ok, n_desc, n_slow, elo);
 }
 
 struct Workspace {
@@ -301,7 +336,8 @@ extern "C" int b2o_exact_sum_f32_ws(const float *x, int64_t n, float s0, float *
   const int gb = (int)std::min<int64_t>(148 * 8, (n + 255) / 256);
   xs_bound_kernel<<<gb, 256, 0, st>>>(x, n, bound);
   xs_summ_kernel<<<(unsigned)nsupers, 1024, 0, st>>>(x, n, bound, s0, chunks, supers, nchunks);
-  xs_compose_kernel<<<1, 32, 0, st>>>(x, n, bound, s0, chunks, supers, nchunks, nsupers, s_out);
+  static const int stats = getenv("B2O_XSUM_STATS") != nullptr;
+  xs_compose_kernel<<<1, 32, 0, st>>>(x, n, bound, s0, chunks, supers, nchunks, nsupers, s_out, stats);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_reductions.py tests/test_xsum_gpu.py -m gpu -x -q > gpurun_out/pytest_red.log 2>&1
-timeout 300 python tools/e2e_trace.py > gpurun_out/e2e_red.log 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 10 --warmup 3 --ops 0 > gpurun_out/bench_n2.log 2>&1
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_quick.log 2>&1
