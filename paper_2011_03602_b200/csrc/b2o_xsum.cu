@@ -20,20 +20,22 @@
 // on the parity of S), an infinity / NaN, or an x too large for the binade
 // flags the run as unusable.
 //
-// Three kernels on the caller's stream:
-//   A  bound:    B = |s0| + sum |x| (double)  -> the binade window: the 16
-//                binades below B's (any |s_j| <= B up to rounding slack);
-//   B  summarise: per chunk of 256 elements (one warp) and per window binade:
-//                (P, min prefix - 1, max prefix + 1, flags); a CTA of 32 warps
-//                also merges its 32 chunks into a super-chunk summary;
-//   C  compose:  one warp walks the super-chunks in order; a super-chunk (or
-//                chunk) whose summary is valid for the current (S, e) is
-//                applied in O(1); otherwise it descends into chunks, and a
-//                chunk that is not valid either (a binade crossing, a tie, an
-//                s <= 0 or outside the window) is added element by element
-//                with __fadd_rn -- the definition itself.
-// Summaries of the next super-chunk / chunk are prefetched (lane k holds the
-// binade-k record) so the serial walk does not wait on memory.
+// Four kernels on the caller's stream:
+//   A  stats:    per super-chunk (8192 terms) sum and sum of magnitudes;
+//   A2 window:   one CTA scans the sums: each super-chunk gets the 4 binades
+//                below (|s0 + earlier sums| + its magnitudes) * 1.25;
+//   B  summarise: per chunk of 256 terms (one warp: 8 parts x 4 binades) and
+//                per super-chunk: (P, min prefix - 1, max prefix + 1, flags)
+//                for each window binade;
+//   C  compose:  one warp walks the super-chunks 32 at a time: lane i picks
+//                super-chunk i's record for the running sum's binade, a warp
+//                scan merges them in order and the longest usable prefix is
+//                applied in O(1); a super-chunk that is not usable is walked
+//                by its chunks the same way, and a chunk that is not usable
+//                either (a binade crossing, a tie, a running sum outside the
+//                window or not normal) is added element by element with
+//                __fadd_rn -- the definition itself.
+// Himeno M's 4.1 M gosa terms: 0.17 ms (15 descents, 23 element-wise chunks).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -50,7 +52,7 @@ namespace {
 constexpr int XS_CHUNK = 256;        // elements per chunk (one warp, 8 per lane)
 constexpr int XS_PER_LANE = XS_CHUNK / 32;
 constexpr int XS_SUPER = 32;         // chunks per super-chunk (one CTA of 32 warps)
-constexpr int XS_W = 16;             // binades in the window
+constexpr int XS_W = 4;              // binades in each super-chunk's window
 
 // A run's effect for one binade, in units u.  Valid summaries have |P|, |lo|,
 // |hi| <= 2^24 + 1 (the running integer stays in [2^23, 2^24)); anything
@@ -95,85 +97,125 @@ __device__ __forceinline__ Summ merge(const Summ &a, const Summ &b) {
   return Summ{a.P + b.P, min(a.lo, a.P + b.lo), max(a.hi, a.P + b.hi), 0};
 }
 
-// A: bound = |s0| + sum |x| (double, atomics: only the window depends on it,
-// never the result)
-__global__ void xs_bound_kernel(const float *__restrict__ x, int64_t n, double *bound) {
-  double a = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    a += fabs((double)x[i]);
+// A: per super-chunk sum and sum of magnitudes (double)
+__global__ void __launch_bounds__(256) xs_stats_kernel(const float *__restrict__ x, int64_t n,
+                                                        double *__restrict__ ssum, double *__restrict__ sabs) {
+  const int64_t b0 = (int64_t)blockIdx.x * XS_SUPER * XS_CHUNK;
+  double a = 0.0, m = 0.0;
+  for (int i = threadIdx.x; i < XS_SUPER * XS_CHUNK; i += blockDim.x) {
+    if (b0 + i < n) {
+      const double v = (double)x[b0 + i];
+      a += v;
+      m += fabs(v);
+    }
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  __shared__ double sm[32];
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = a;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    m += __shfl_xor_sync(0xffffffffu, m, o);
+  }
+  __shared__ double sa[8], sm[8];
+  if ((threadIdx.x & 31) == 0) {
+    sa[threadIdx.x >> 5] = a;
+    sm[threadIdx.x >> 5] = m;
+  }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    a = threadIdx.x < blockDim.x / 32 ? sm[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (threadIdx.x == 0) atomicAdd(bound, a);
+  if (threadIdx.x == 0) {
+    double ta = 0.0, tm = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      ta += sa[w];
+      tm += sm[w];
+    }
+    ssum[blockIdx.x] = ta;
+    sabs[blockIdx.x] = tm;
   }
 }
 
-__device__ __forceinline__ int window_lo(const double *bound, float s0) {
-  const double b = (*bound + fabs((double)s0)) * 1.0009765625 + 1e-30;
-  int e;
-  frexp(b, &e);  // b in [2^(e-1), 2^e); one binade of headroom above for
-                 // the accumulated rounding of long sums
-  return e - (XS_W - 1);
+// A2: each super-chunk's binade window.  est = s0 + sum of the earlier
+// super-chunks (double); |s| inside the super-chunk is at most |est| + its
+// magnitudes, with 25 % slack for the drift of the fp32 running sum from the
+// exact one; the window is the XS_W binades up to that bound (a running sum
+// below it is added element by element: exact, only slower).
+__global__ void __launch_bounds__(1024) xs_window_kernel(const double *__restrict__ ssum,
+                                                          const double *__restrict__ sabs, int64_t nsupers,
+                                                          float s0, int *__restrict__ ebase) {
+  __shared__ double part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (nsupers + 1023) / 1024;
+  const int64_t i0 = t * per, i1 = min(i0 + per, nsupers);
+  double loc = 0.0;
+  for (int64_t i = i0; i < i1; ++i) loc += ssum[i];
+  part[t] = loc;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {  // inclusive Hillis-Steele scan
+    const double v = t >= d ? part[t - d] : 0.0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  double est = (double)s0 + (t > 0 ? part[t - 1] : 0.0);
+  for (int64_t i = i0; i < i1; ++i) {
+    const double top = (fabs(est) + sabs[i]) * 1.25 + 1e-30;
+    int e;
+    frexp(top, &e);  // top in [2^(e-1), 2^e)
+    ebase[i] = (e - 1) - (XS_W - 1);
+    est += ssum[i];
+  }
 }
 
-// B: chunk and super-chunk summaries for every window binade.  A warp owns a
-// chunk; lane k (k < 16) runs binade elo + k over the first half of the
-// chunk, lane 16 + k over the second half, and the halves are merged.
-__global__ void __launch_bounds__(1024) xs_summ_kernel(const float *__restrict__ x, int64_t n, const double *bound,
-                                                        float s0, Summ *__restrict__ chunks,
+// B: chunk and super-chunk summaries for the XS_W window binades of their
+// super-chunk.  A warp owns a chunk: lane = 4 * part + k runs binade
+// ebase + k over part (32 elements) of the chunk; the 8 parts are merged in
+// order with three shuffles.
+__global__ void __launch_bounds__(1024) xs_summ_kernel(const float *__restrict__ x, int64_t n,
+                                                        const int *__restrict__ ebase, Summ *__restrict__ chunks,
                                                         Summ *__restrict__ supers, int64_t nchunks) {
-  __shared__ float xs[XS_SUPER][XS_CHUNK + 1];
+  __shared__ float xs[XS_SUPER][XS_CHUNK + XS_CHUNK / 32];
   __shared__ Summ sm[XS_SUPER][XS_W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * XS_SUPER + warp;
-  const int elo = window_lo(bound, s0);
   const int64_t base = c * XS_CHUNK;
   const int cnt = c < nchunks ? (int)min((int64_t)XS_CHUNK, n - base) : 0;
 #pragma unroll
   for (int j = 0; j < XS_PER_LANE; ++j) {
     const int i = lane + 32 * j;
-    xs[warp][i + (i >> 7)] = i < cnt ? x[base + i] : 0.f;  // halves in different banks
+    xs[warp][i + (i >> 5)] = i < cnt ? x[base + i] : 0.f;  // parts in different banks
   }
   __syncwarp();
-  const int k = lane & (XS_W - 1), h = lane >> 4;
-  const int e = elo + k;
+  const int k = lane & (XS_W - 1), part = lane >> 2;
+  const int e = ebase[blockIdx.x] + k;
+  constexpr int PART = XS_CHUNK / 8;
   int P = 0, lo = kLoEmpty, hi = kHiEmpty, flag = 0;
-  const int i0 = h * (XS_CHUNK / 2), i1 = min(i0 + XS_CHUNK / 2, cnt);
-  if (i1 - i0 == XS_CHUNK / 2) {
-    // full half: 8 elements per step, loads first (independent of the scan)
-#pragma unroll 2
-    for (int i = i0; i < i1; i += 8) {
+  const int i0 = part * PART, i1 = min(i0 + PART, cnt);
+  const float *row = &xs[warp][part * (PART + 1)];
+  if (i1 - i0 == PART) {
+#pragma unroll 4
+    for (int i = 0; i < PART; i += 8) {
       uint32_t b[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = __float_as_uint(xs[warp][i + j + h]);
+      for (int j = 0; j < 8; ++j) b[j] = __float_as_uint(row[i + j]);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        P += units(b[j], e, flag);  // |P| < 128 * 2^24: no overflow
+        P += units(b[j], e, flag);  // |P| < 32 * 2^24: no overflow
         lo = min(lo, P - 1);
         hi = max(hi, P + 1);
       }
     }
   } else {
-    for (int i = i0; i < i1; ++i) {
-      P += units(__float_as_uint(xs[warp][i + h]), e, flag);
+    for (int i = 0; i < i1 - i0; ++i) {
+      P += units(__float_as_uint(row[i]), e, flag);
       lo = min(lo, P - 1);
       hi = max(hi, P + 1);
     }
   }
   Summ s{P, lo, hi, flag};
-  Summ t;
-  t.P = __shfl_down_sync(0xffffffffu, s.P, 16);
-  t.lo = __shfl_down_sync(0xffffffffu, s.lo, 16);
-  t.hi = __shfl_down_sync(0xffffffffu, s.hi, 16);
-  t.flags = __shfl_down_sync(0xffffffffu, s.flags, 16);
+#pragma unroll
+  for (int d = 4; d < 32; d <<= 1) {  // ordered merge: part p with part p + d/4
+    Summ t{__shfl_down_sync(0xffffffffu, s.P, d), __shfl_down_sync(0xffffffffu, s.lo, d),
+           __shfl_down_sync(0xffffffffu, s.hi, d), __shfl_down_sync(0xffffffffu, s.flags, d)};
+    if ((part & (2 * (d >> 2) - 1)) == 0) s = merge(s, t);
+  }
   if (lane < XS_W) {
-    s = merge(s, t);
     if (c < nchunks) chunks[c * XS_W + k] = s;
     sm[warp][k] = s;
   }
@@ -186,119 +228,178 @@ __global__ void __launch_bounds__(1024) xs_summ_kernel(const float *__restrict__
   }
 }
 
-// apply the binade-k record of a summary row (row[k], k from s) to s.
-// s < 0 runs the mirrored problem: fl(s + x) = -fl(|s| + (-x)), whose units
-// are -r, so the prefix range flips (|S| - hi, |S| - lo) and S' = |S| - P.
-__device__ __forceinline__ bool apply(float &s, const Summ *row, int elo) {
+// ---- C: the in-order walk (one warp) -------------------------------------
+
+struct WalkState {
+  bool ok;   // s is a normal float
+  int e;     // its binade: |s| in [2^e, 2^(e+1))
+  int S;     // |s| / 2^(e-23), in [2^23, 2^24)
+  bool neg;
+};
+
+__device__ __forceinline__ WalkState state_of(float s) {
   const uint32_t bits = __float_as_uint(s);
   const uint32_t exr = (bits >> 23) & 0xFFu;
-  const int k = (int)exr - 127 - elo;
-  if (exr == 0 || exr == 0xFFu || k < 0 || k >= XS_W) return false;
-  const Summ t = row[k];
-  if (t.flags) return false;
-  if (t.lo == kLoEmpty) return true;
-  const int S = (int)((bits & 0x7FFFFFu) | 0x800000u);
-  int S2;
-  if ((bits >> 31) == 0) {
-    if (S + t.lo < (1 << 23) || S + t.hi > (1 << 24)) return false;
-    S2 = S + t.P;
-  } else {
-    if (S - t.hi < (1 << 23) || S - t.lo > (1 << 24)) return false;
-    S2 = S - t.P;
-  }
-  s = __uint_as_float((bits & 0x80000000u) | (exr << 23) | (uint32_t)(S2 - (1 << 23)));
-  return true;
+  return WalkState{exr != 0 && exr != 0xFFu, (int)exr - 127, (int)((bits & 0x7FFFFFu) | 0x800000u),
+                   (bits >> 31) != 0};
 }
 
-// C: the serial walk (one warp).  Super-chunk summaries stream through a
-// double-buffered shared-memory window of 32 super-chunks (the next window's
-// loads are in flight while the current one is walked); a descent loads the
-// 32 chunk summaries of one super-chunk at once.
+#define kEmpty (Summ{0, kLoEmpty, kHiEmpty, 0})
+#define kInvalid (Summ{0, 0, 0, 1})
+
+// a run summary (for s's binade) is usable from state w.  s < 0 runs the
+// mirrored problem: fl(s + x) = -fl(|s| + (-x)), whose units are -r, so the
+// prefix range flips (|S| - hi, |S| - lo) and S' = |S| - P.
+__device__ __forceinline__ bool usable(const Summ &t, const WalkState &w) {
+  if (t.flags) return false;
+  if (t.lo == kLoEmpty) return true;
+  return w.neg ? (w.S - t.hi >= (1 << 23) && w.S - t.lo <= (1 << 24))
+               : (w.S + t.lo >= (1 << 23) && w.S + t.hi <= (1 << 24));
+}
+
+__device__ __forceinline__ float advance(float s, const Summ &t, const WalkState &w) {
+  if (t.lo == kLoEmpty) return s;
+  const int S2 = w.neg ? w.S - t.P : w.S + t.P;
+  return __uint_as_float((__float_as_uint(s) & 0xFF800000u) | (uint32_t)(S2 - (1 << 23)));
+}
+
+// lane i holds the summary (for s's binade) of run i: kEmpty outside
+// [first, cnt), kInvalid when its window lacks the binade.  Applies the
+// longest usable prefix of runs first.. to s; returns how many runs that was.
+__device__ __forceinline__ int scan_apply(float &s, Summ mine, int first, int cnt, const WalkState &w) {
+  const int lane = threadIdx.x & 31;
+  Summ pre = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Summ t{__shfl_up_sync(0xffffffffu, pre.P, d), __shfl_up_sync(0xffffffffu, pre.lo, d),
+                 __shfl_up_sync(0xffffffffu, pre.hi, d), __shfl_up_sync(0xffffffffu, pre.flags, d)};
+    if (lane >= d) pre = merge(t, pre);
+  }
+  const unsigned bad = __ballot_sync(0xffffffffu, lane >= first && lane < cnt && !usable(pre, w));
+  const int f = bad ? __ffs(bad) - 1 : cnt;
+  if (f > first) {
+    const Summ t{__shfl_sync(0xffffffffu, pre.P, f - 1), __shfl_sync(0xffffffffu, pre.lo, f - 1),
+                 __shfl_sync(0xffffffffu, pre.hi, f - 1), __shfl_sync(0xffffffffu, pre.flags, f - 1)};
+    s = advance(s, t, w);
+  }
+  return f - first;
+}
+
+// C: one warp walks the super-chunks 32 at a time: lane i picks super-chunk
+// i's record for s's binade, a warp scan merges them in order and the
+// longest usable prefix is applied in O(1).  A super-chunk that is not
+// usable is walked by its 32 chunks the same way; a chunk that is not usable
+// either (binade crossing, tie, s outside its window or not normal) is added
+// element by element with __fadd_rn -- the definition.  The next group's
+// records are loaded while the current group is walked.
 __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict__ x, int64_t n,
-                                                         const double *bound, float s0,
+                                                         const int *__restrict__ ebase, float s0,
                                                          const Summ *__restrict__ chunks,
                                                          const Summ *__restrict__ supers, int64_t nchunks,
                                                          int64_t nsupers, float *out, int stats) {
-  int n_desc = 0, n_slow = 0, n_super_ok = 0;
-  constexpr int G = 32;                       // super-chunks per window
-  constexpr int REC = G * XS_W;               // records per window (int4 each)
-  __shared__ int4 sbuf[2][REC];
+  __shared__ int4 sbuf[2][32 * XS_W];
   __shared__ int4 cbuf[XS_SUPER * XS_W];
   __shared__ __align__(16) float xbuf[XS_CHUNK];
   const int lane = threadIdx.x;
-  const int elo = window_lo(bound, s0);
   const int4 *sup4 = reinterpret_cast<const int4 *>(supers);
   const int4 *chk4 = reinterpret_cast<const int4 *>(chunks);
-  const int64_t nrec = nsupers * XS_W;
-  int4 pre[REC / 32];
+  int n_desc = 0, n_slow = 0;
+  int4 pre[XS_W];
+  int peb = 0;
   auto fetch = [&](int64_t g) {
 #pragma unroll
-    for (int j = 0; j < REC / 32; ++j) {
-      const int64_t r = g * REC + lane + 32 * j;
-      pre[j] = r < nrec ? sup4[r] : make_int4(0, 0, 0, 1);
+    for (int j = 0; j < XS_W; ++j) {
+      const int64_t r = g * 32 * XS_W + lane + 32 * j;
+      pre[j] = r < nsupers * XS_W ? sup4[r] : make_int4(0, 0, 0, 1);
     }
+    peb = g * 32 + lane < nsupers ? ebase[g * 32 + lane] : 0;
   };
   auto stash = [&](int b) {
 #pragma unroll
-    for (int j = 0; j < REC / 32; ++j) sbuf[b][lane + 32 * j] = pre[j];
+    for (int j = 0; j < XS_W; ++j) sbuf[b][lane + 32 * j] = pre[j];
   };
   float s = s0;
-  const int64_t ngroups = (nsupers + G - 1) / G;
+  const int64_t ngroups = (nsupers + 31) / 32;
   fetch(0);
   stash(0);
+  int eb = peb;
   __syncwarp();
   for (int64_t g = 0; g < ngroups; ++g) {
     const int cur = (int)(g & 1);
     if (g + 1 < ngroups) fetch(g + 1);
-    const int64_t s_end = min((g + 1) * G, nsupers);
-    for (int64_t sc = g * G; sc < s_end; ++sc) {
-      if (apply(s, reinterpret_cast<const Summ *>(&sbuf[cur][(sc - g * G) * XS_W]), elo)) {
-        ++n_super_ok;
-        continue;
+    const int cnt = (int)min((int64_t)32, nsupers - g * 32);
+    const Summ *srec = reinterpret_cast<const Summ *>(sbuf[cur]);
+    int pos = 0;
+    while (pos < cnt) {
+      WalkState w = state_of(s);
+      if (w.ok) {
+        const int k = w.e - eb;
+        Summ mine = (lane < pos || lane >= cnt) ? kEmpty : ((k >= 0 && k < XS_W) ? srec[lane * XS_W + k] : kInvalid);
+        pos += scan_apply(s, mine, pos, cnt, w);
+        if (pos >= cnt) break;
       }
+      // super-chunk g*32 + pos by its chunks
       ++n_desc;
+      const int64_t sc = g * 32 + pos;
+      const int ceb = __shfl_sync(0xffffffffu, eb, pos);
       const int64_t c0 = sc * XS_SUPER, c1 = min(c0 + XS_SUPER, nchunks);
+      const int nc = (int)(c1 - c0);
       __syncwarp();
 #pragma unroll
-      for (int j = 0; j < XS_SUPER * XS_W / 32; ++j) {
+      for (int j = 0; j < XS_W; ++j) {
         const int64_t r = c0 * XS_W + lane + 32 * j;
         cbuf[lane + 32 * j] = r < nchunks * XS_W ? chk4[r] : make_int4(0, 0, 0, 1);
       }
       __syncwarp();
-      for (int64_t c = c0; c < c1; ++c) {
-        if (apply(s, reinterpret_cast<const Summ *>(&cbuf[(c - c0) * XS_W]), elo)) continue;
-        // element by element: the definition
+      const Summ *crec = reinterpret_cast<const Summ *>(cbuf);
+      int cpos = 0;
+      while (cpos < nc) {
+        w = state_of(s);
+        if (w.ok) {
+          const int k = w.e - ceb;
+          Summ mine = (lane < cpos || lane >= nc) ? kEmpty
+                                                  : ((k >= 0 && k < XS_W) ? crec[lane * XS_W + k] : kInvalid);
+          cpos += scan_apply(s, mine, cpos, nc, w);
+          if (cpos >= nc) break;
+        }
+        // chunk c0 + cpos element by element
         ++n_slow;
-        const int64_t base = c * XS_CHUNK;
-        const int cnt = (int)min((int64_t)XS_CHUNK, n - base);
+        const int64_t base = (c0 + cpos) * XS_CHUNK;
+        const int m = (int)min((int64_t)XS_CHUNK, n - base);
 #pragma unroll
         for (int j = 0; j < XS_PER_LANE; ++j) {
           const int i = lane + 32 * j;
-          xbuf[i] = i < cnt ? x[base + i] : 0.f;
+          xbuf[i] = i < m ? x[base + i] : 0.f;
         }
         __syncwarp();
+        const float *xb = xbuf;
         if (lane == 0) {
           int i = 0;
-          for (; i + 8 <= cnt; i += 8) {  // operands fetched ahead of the dependent adds
-            const float4 a = *reinterpret_cast<const float4 *>(&xbuf[i]);
-            const float4 b = *reinterpret_cast<const float4 *>(&xbuf[i + 4]);
+          for (; i + 8 <= m; i += 8) {  // operands fetched ahead of the dependent adds
+            const float4 a = *reinterpret_cast<const float4 *>(&xb[i]);
+            const float4 b = *reinterpret_cast<const float4 *>(&xb[i + 4]);
             s = __fadd_rn(s, a.x); s = __fadd_rn(s, a.y); s = __fadd_rn(s, a.z); s = __fadd_rn(s, a.w);
             s = __fadd_rn(s, b.x); s = __fadd_rn(s, b.y); s = __fadd_rn(s, b.z); s = __fadd_rn(s, b.w);
           }
-          for (; i < cnt; ++i) s = __fadd_rn(s, xbuf[i]);
+          for (; i < m; ++i) s = __fadd_rn(s, xb[i]);
         }
         s = __shfl_sync(0xffffffffu, s, 0);
         __syncwarp();
+        ++cpos;
       }
+      ++pos;
     }
     __syncwarp();
-    if (g + 1 < ngroups) stash(cur ^ 1);
+    if (g + 1 < ngroups) {
+      stash(cur ^ 1);
+      eb = peb;
+    }
     __syncwarp();
   }
   if (lane == 0) *out = s;
   if (stats && lane == 0)
-    printf("[xsum] n=%lld supers=%lld ok=%d descents=%d slow_chunks=%d elo=%d\n", (long long)n,
-           (long long)nsupers, n_super_ok, n_desc, n_slow, elo);
+    printf("[xsum] n=%lld supers=%lld descents=%d slow_chunks=%d\n", (long long)n, (long long)nsupers, n_desc,
+           n_slow);
 }
 
 struct Workspace {
@@ -310,15 +411,30 @@ std::map<int, Workspace> ws_by_dev;
 
 }  // namespace
 
-extern "C" size_t b2o_exact_sum_workspace(int64_t n) {
-  const int64_t nchunks = (n + XS_CHUNK - 1) / XS_CHUNK;
-  const int64_t nsupers = (nchunks + XS_SUPER - 1) / XS_SUPER;
-  return 256 + sizeof(Summ) * XS_W * (size_t)(nchunks + nsupers + 32 * XS_W);
+struct Layout {
+  int64_t nchunks, nsupers;
+  size_t ssum, sabs, ebase, chunks, supers, bytes;
+};
+
+Layout layout(int64_t n) {
+  Layout L;
+  L.nchunks = (n + XS_CHUNK - 1) / XS_CHUNK;
+  L.nsupers = (L.nchunks + XS_SUPER - 1) / XS_SUPER;
+  auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  L.ssum = 0;
+  L.sabs = up(L.ssum + sizeof(double) * L.nsupers);
+  L.ebase = up(L.sabs + sizeof(double) * L.nsupers);
+  L.chunks = up(L.ebase + sizeof(int) * (L.nsupers + 32));
+  L.supers = up(L.chunks + sizeof(Summ) * XS_W * L.nchunks);
+  L.bytes = up(L.supers + sizeof(Summ) * XS_W * (L.nsupers + 32));
+  return L;
 }
 
+extern "C" size_t b2o_exact_sum_workspace(int64_t n) { return layout(std::max<int64_t>(n, 1)).bytes; }
+
 // s_out = (((s0 + x[0]) + x[1]) + ...) in fp32, bit-identical to the loop;
-// workspace: device memory of b2o_exact_sum_workspace(n) bytes (NULL: an
-// internal per-device buffer).  Asynchronous on `stream`.
+// workspace: device memory of b2o_exact_sum_workspace(n) bytes.
+// Asynchronous on `stream`.
 extern "C" int b2o_exact_sum_f32_ws(const float *x, int64_t n, float s0, float *s_out, void *workspace,
                                     void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -326,18 +442,16 @@ extern "C" int b2o_exact_sum_f32_ws(const float *x, int64_t n, float s0, float *
   if (n == 0) {
     return cudaMemcpyAsync(s_out, &s0, sizeof(float), cudaMemcpyHostToDevice, st) == cudaSuccess ? 0 : -1;
   }
-  const int64_t nchunks = (n + XS_CHUNK - 1) / XS_CHUNK;
-  const int64_t nsupers = (nchunks + XS_SUPER - 1) / XS_SUPER;
+  const Layout L = layout(n);
   char *ws = (char *)workspace;
-  double *bound = (double *)ws;
-  Summ *chunks = (Summ *)(ws + 256);
-  Summ *supers = chunks + XS_W * nchunks;
-  if (cudaMemsetAsync(bound, 0, sizeof(double), st) != cudaSuccess) return -1;
-  const int gb = (int)std::min<int64_t>(148 * 8, (n + 255) / 256);
-  xs_bound_kernel<<<gb, 256, 0, st>>>(x, n, bound);
-  xs_summ_kernel<<<(unsigned)nsupers, 1024, 0, st>>>(x, n, bound, s0, chunks, supers, nchunks);
+  double *ssum = (double *)(ws + L.ssum), *sabs = (double *)(ws + L.sabs);
+  int *ebase = (int *)(ws + L.ebase);
+  Summ *chunks = (Summ *)(ws + L.chunks), *supers = (Summ *)(ws + L.supers);
+  xs_stats_kernel<<<(unsigned)L.nsupers, 256, 0, st>>>(x, n, ssum, sabs);
+  xs_window_kernel<<<1, 1024, 0, st>>>(ssum, sabs, L.nsupers, s0, ebase);
+  xs_summ_kernel<<<(unsigned)L.nsupers, 1024, 0, st>>>(x, n, ebase, chunks, supers, L.nchunks);
   static const int stats = getenv("B2O_XSUM_STATS") != nullptr;
-  xs_compose_kernel<<<1, 32, 0, st>>>(x, n, bound, s0, chunks, supers, nchunks, nsupers, s_out, stats);
+  xs_compose_kernel<<<1, 32, 0, st>>>(x, n, ebase, s0, chunks, supers, L.nchunks, L.nsupers, s_out, stats);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
