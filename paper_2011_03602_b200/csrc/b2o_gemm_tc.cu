@@ -576,6 +576,59 @@ __global__ void zero_tiles_kernel(float *__restrict__ C, int N, int tiles_m, int
   for (int j = threadIdx.x; j < BN / 4; j += blockDim.x) d[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+// One launch for all operand preparation of the pair kernel (no gaps
+// between dependent prep kernels): blocks [0, nA) split A (float4, grid-
+// stride), the next nB blocks split + transpose 64 x 64 tiles of B, the rest
+// zero the K-split tail tiles of C (8 rows of one tile per block).
+constexpr int PREP_T = 64;
+__global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ A, const float *__restrict__ B,
+                                                   float *__restrict__ Ah, float *__restrict__ Al,
+                                                   float *__restrict__ BhT, float *__restrict__ BlT, int K, int N,
+                                                   size_t a4, int mode, int nA, int nBx, int nB, float *__restrict__ C,
+                                                   int tiles_m, int first_tile) {
+  __shared__ float tile[PREP_T][PREP_T + 1];
+  const int b = blockIdx.x;
+  if (b < nA) {
+    const float4 *x = reinterpret_cast<const float4 *>(A);
+    float4 *h4 = reinterpret_cast<float4 *>(Ah), *l4 = reinterpret_cast<float4 *>(Al);
+    for (size_t i = (size_t)b * blockDim.x + threadIdx.x; i < a4; i += (size_t)nA * blockDim.x) {
+      const float4 v = x[i];
+      float4 h, l;
+      split_value(v.x, mode, h.x, l.x);
+      split_value(v.y, mode, h.y, l.y);
+      split_value(v.z, mode, h.z, l.z);
+      split_value(v.w, mode, h.w, l.w);
+      h4[i] = h;
+      l4[i] = l;
+    }
+    return;
+  }
+  if (b < nA + nB) {
+    const int t = b - nA;
+    const int n0 = (t % nBx) * PREP_T, k0 = (t / nBx) * PREP_T;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    for (int r = ty; r < PREP_T; r += 4) tile[r][tx] = B[(size_t)(k0 + r) * N + n0 + tx];
+    __syncthreads();
+    for (int r = ty; r < PREP_T; r += 4) {
+      float h, l;
+      split_value(tile[tx][r], mode, h, l);
+      const size_t o = (size_t)(n0 + r) * K + k0 + tx;
+      BhT[o] = h;
+      BlT[o] = l;
+    }
+    return;
+  }
+  // zero 8 rows of a K-split tail tile
+  const int z = b - nA - nB;
+  const int tile_i = first_tile + z / (2 * BM / 8);
+  const int m0 = (tile_i % tiles_m) * (2 * BM), n0 = (tile_i / tiles_m) * BN;
+  const int r0 = m0 + (z % (2 * BM / 8)) * 8;
+  for (int j = threadIdx.x; j < 8 * BN / 4; j += blockDim.x) {
+    float4 *d = (float4 *)(C + (size_t)(r0 + j / (BN / 4)) * N + n0);
+    d[j % (BN / 4)] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 }  // namespace pair
 
 // ---------------------------------------------------------------------------
@@ -653,15 +706,19 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
   float *Ah = ws, *Al = ws + a_elems, *Bh = Al + a_elems, *Bl = Bh + b_elems;
   static const int split_mode = getenv("B2O_GEMM_SPLIT") ? atoi(getenv("B2O_GEMM_SPLIT")) : 0;
   if (phase_ev) cudaEventRecord(phase_ev[0], s);
-  split_kernel<<<148 * 8, 256, 0, s>>>(A, Ah, Al, a_elems, split_mode);
-  dim3 tg((unsigned)(n / 32), (unsigned)(k / 32));
-  split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bh, Bl, (int)k, (int)n, split_mode);
-  if (phase_ev) cudaEventRecord(phase_ev[1], s);
   CUtensorMap mAh, mAl, mBh, mBl;
   int dev = 0;
   cudaGetDevice(&dev);
   static const bool force_1cta = getenv("B2O_GEMM_1CTA") != nullptr;
-  if (m % (2 * pair::BM) == 0 && n % pair::BN == 0 && !force_1cta) {
+  static const bool split_prep = getenv("B2O_GEMM_SPLIT_PREP") != nullptr;  // the two-kernel prep (A/B)
+  const bool pair_path = m % (2 * pair::BM) == 0 && n % pair::BN == 0 && !force_1cta;
+  if (!pair_path || split_prep || n % pair::PREP_T || k % pair::PREP_T) {
+    split_kernel<<<148 * 8, 256, 0, s>>>(A, Ah, Al, a_elems, split_mode);
+    dim3 tg((unsigned)(n / 32), (unsigned)(k / 32));
+    split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bh, Bl, (int)k, (int)n, split_mode);
+    if (!pair_path && phase_ev) cudaEventRecord(phase_ev[1], s);
+  }
+  if (pair_path) {
     // CTA pairs: each CTA maps 128 rows of A and 128 rows (= N columns) of B^T
     if (!make_map(&mAh, Ah, (int)m, (int)k, pair::BM) || !make_map(&mAl, Al, (int)m, (int)k, pair::BM) ||
         !make_map(&mBh, Bh, (int)n, (int)k, pair::BNH) || !make_map(&mBl, Bl, (int)n, (int)k, pair::BNH))
@@ -683,9 +740,16 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
     sc.rem = sc.T % sc.P;
     sc.nchunks = (int)((k / pair::BK + pair::KCHUNK_BLOCKS - 1) / pair::KCHUNK_BLOCKS);
     sc.S = (sc.rem > 0 && 2 * sc.rem <= sc.P && sc.nchunks >= 2 && !getenv("B2O_GEMM_NOSPLIT")) ? 2 : 1;
-    if (sc.S == 2) {
+    if (!split_prep && n % pair::PREP_T == 0 && k % pair::PREP_T == 0) {
+      const int nA = 148 * 8;
+      const int nBx = (int)(n / pair::PREP_T), nB = nBx * (int)(k / pair::PREP_T);
+      const int nZ = sc.S == 2 ? sc.rem * (2 * pair::BM / 8) : 0;
+      pair::prep_kernel<<<nA + nB + nZ, 256, 0, s>>>(A, B, Ah, Al, Bh, Bl, (int)k, (int)n, a_elems / 4, split_mode,
+                                                    nA, nBx, nB, C, sc.tiles_m, sc.waves * sc.P);
+    } else if (sc.S == 2) {
       pair::zero_tiles_kernel<<<dim3(2 * pair::BM, sc.rem), 64, 0, s>>>(C, (int)n, sc.tiles_m, sc.waves * sc.P);
     }
+    if (phase_ev) cudaEventRecord(phase_ev[1], s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * sc.P));
     cfg.blockDim = dim3(pair::THREADS);
