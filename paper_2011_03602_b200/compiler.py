@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-27"
+COMPILER_VERSION = "b2o-compiler-28"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -644,30 +644,53 @@ class _Gen:
     def exact_reductions(self, n: NestPlan) -> dict:
         """Reductions of a chained nest that can be summed EXACTLY in loop
         order on the GPU (b2o_exact_sum_f32, csrc/b2o_xsum.cu): an fp32 scalar
-        updated by ``s = s + e`` / ``s = e + s`` / ``s = s - e`` with ``e`` of
-        C type float (so the C statement is one fp32 addition), exactly once
-        per point: the statement sits directly in the innermost chain loop's
-        body and is the nest's only update of ``s``.  The kernel stores the
-        per-point terms in loop order, the runtime reproduces the sequential
-        sum bit for bit.  spec ``exact_reductions: false`` keeps the
-        reassociating tree (faster, documented tolerance).  Returns
-        ``{var: slot}``."""
+        whose every update in the nest is ``s = s + e`` / ``s = e + s`` /
+        ``s = s - e`` with ``e`` of C type float (one fp32 addition each), and
+        which every point of the chain updates a compile-time constant
+        number of times C (the loops run in-thread below the chain have
+        literal bounds).  Point t's j-th update stores its term at
+        ``t * C + j``: the buffer holds the terms in sequential loop order and
+        the runtime reproduces the sequential sum bit for bit.  spec
+        ``exact_reductions: false`` keeps the reassociating tree (faster,
+        documented tolerance).  Returns ``{var: (slot, C)}``."""
         if not n.reds or not n.chain or self.spec.get("exact_reductions") is False:
             return {}
         prog = self.prog
-        body = prog.regions[prog.loops[n.chain[-1]].body].statements
+
+        def count(rid, v):
+            total = 0
+            for st in prog.regions[rid].statements:
+                if st.kind == "assign" and st.target[0] == "var" and st.target[1] == v:
+                    red = reductions.reduction_stmt(st)
+                    if red is None or etype(prog, red[2], self.precision) != "float":
+                        return None
+                    total += 1
+                elif st.kind == "loop":
+                    lp = prog.loops[st.loop]
+                    if lp.lower[0] != "num" or lp.upper[0] != "num" or lp.lower[2] or lp.upper[2]:
+                        if any(x.kind == "assign" and x.target[0] == "var" and x.target[1] == v
+                               for x in prog.walk(lp.body)):
+                            return None
+                        continue
+                    c = count(lp.body, v)
+                    if c is None:
+                        return None
+                    total += c * max(0, int(lp.upper[1]) - int(lp.lower[1]))
+                elif st.kind == "call" and not prog.is_opaque_call(st.call):
+                    c = count(prog.calls[st.call].subtree, v)  # inlined body (dev_region recurses too)
+                    if c is None:
+                        return None
+                    total += c
+            return total
+
         out = {}
         for v in sorted(n.reds):
             if self.T(v) != "float":
                 continue
-            hits = [st for st in prog.walk(prog.loops[n.root].body)
-                    if st.kind == "assign" and st.target[0] == "var" and st.target[1] == v]
-            if len(hits) != 1 or hits[0] not in body:
+            c = count(prog.loops[n.chain[-1]].body, v)
+            if not c:
                 continue
-            red = reductions.reduction_stmt(hits[0])
-            if red is None or etype(prog, red[2], self.precision) != "float":
-                continue
-            out[v] = len(out)
+            out[v] = (len(out), c)
         return out
 
     def exact_elems(self) -> int:
@@ -685,7 +708,7 @@ class _Gen:
                     tot = 0
                     break
                 tot *= max(0, int(hi[1]) - int(lo[1]))
-            best = max(best, tot)
+            best = max(best, tot * max(c for _, c in n.exact.values()))
         return best
 
     # -- helpers -----------------------------------------------------------
@@ -1010,11 +1033,11 @@ class _Gen:
                 cap = min(cap, 2048)  # B2O_RED_MAX_BLOCKS: one partial per CTA in the scratch
             out.append(f"  {{ uint64_t g = (total + {per - 1}) / {per}; geom[0] = (uint32_t)(g > {cap}u ? "
                        f"{cap}u : g); geom[1] = geom[2] = 1; geom[3] = {bt}; geom[4] = geom[5] = 1; }}")
-        for v, slot in (n.exact or {}).items():
-            out.append(f"  a.xb{v} = (float *)ex->red_buf(ex, {slot}, (int64_t)total); if (ex->stop) return;")
+        for v, (slot, cnt) in (n.exact or {}).items():
+            out.append(f"  a.xb{v} = (float *)ex->red_buf(ex, {slot}, (int64_t)total * {cnt}); if (ex->stop) return;")
         out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, geom);")
-        for v, slot in (n.exact or {}).items():
-            out.append(f"  if (!ex->stop) ex->red_exact(ex, {v}, {slot}, (int64_t)total, a.s{v});")
+        for v, (slot, cnt) in (n.exact or {}).items():
+            out.append(f"  if (!ex->stop) ex->red_exact(ex, {v}, {slot}, (int64_t)total * {cnt}, a.s{v});")
         out.append("}")
         return out
 
@@ -1071,6 +1094,9 @@ class _Gen:
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
             out.append(f"    {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        for v, (slot, cnt) in (n.exact or {}).items():
+            if cnt > 1:
+                out.append(f"    uint32_t xc{v} = 0;  // this point's terms of {prog.vars[v].name} so far")
         D = len(n.chain)
         for c in n.chain:
             out.append(f"    int32_t v{prog.loops[c].index_var}_;")
@@ -1915,7 +1941,11 @@ class _Gen:
                     # the term of this point, in loop order (t); s - e == s + (-e) exactly
                     v, op, e = red
                     sign = "-" if op == "-" else ""
-                    out.append(pad + f"a.xb{v}[t] = {sign}(float)({self.dev_expr(e)});")
+                    cnt = self._exact[v][1]
+                    if cnt == 1:
+                        out.append(pad + f"a.xb{v}[t] = {sign}(float)({self.dev_expr(e)});")
+                    else:
+                        out.append(pad + f"a.xb{v}[(size_t)t * {cnt}u + xc{v}++] = {sign}(float)({self.dev_expr(e)});")
                 elif red is not None and red[0] in self._reds:
                     v, op, e = red
                     out.append(pad + f"rd{v} = rd{v} {op} ({self.dev_expr(e)});")

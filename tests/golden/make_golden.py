@@ -148,7 +148,27 @@ def block_record(name: str, model, spec: dict) -> dict:
     }
 
 
+def shapes() -> None:
+    """tests/_fuzz_shapes.py programs (k-tile, plane-march, exact-reduction
+    kernels): all genomes, reference plans; the reduction family under the
+    opt-in screen."""
+    sys.path.insert(0, str(HERE.parent))
+    import _fuzz_shapes
+
+    rec = {}
+    for seed in _fuzz_shapes.SEEDS:
+        m = parse_mini_source(_fuzz_shapes.program(seed))
+        sp = _fuzz_shapes.spec(seed)
+        scr = screen_model_with_reductions if sp.get("reductions") else screen_model
+        rec[str(seed)] = app_record(f"shapes_{seed}", m, sp, all_genomes_cap=512, screen=scr)
+    (HERE / "fuzz_shapes.json").write_text(json.dumps(rec, sort_keys=True) + "\n")
+    print("wrote fuzz_shapes.json:", {k: len(v["patterns"]) for k, v in rec.items()})
+
+
 def main() -> None:
+    if "--shapes" in sys.argv:
+        shapes()
+        return
     out: dict[str, dict] = {}
     for fx in ("four_loops", "nest2d", "stencil", "triple_nest", "matmul", "three_loops_fft"):
         m = parse_mini_source(fixture(f"{fx}.mini"))
@@ -222,6 +242,7 @@ def main() -> None:
         m = parse_mini_source(_fuzz.program(seed))
         fuzz[str(seed)] = app_record(f"fuzz_{seed}", m, _fuzz.spec(seed), all_genomes_cap=256)
     (HERE / "fuzz.json").write_text(json.dumps(fuzz, sort_keys=True) + "\n")
+    shapes()
     print("wrote", sorted(p.name for p in HERE.glob("*.json")))
 
 
