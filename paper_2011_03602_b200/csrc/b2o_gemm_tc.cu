@@ -804,3 +804,16 @@ extern "C" int b2o_gemm_f32_phases(const float *A, const float *B, float *C, int
   for (auto &e : ev) cudaEventDestroy(e);
   return rc;
 }
+
+// force-load this file's kernels (lazy module loading would otherwise charge
+// the first timed pattern that uses one); called per device by b2o_init
+extern "C" void b2o_gemm_tc_warm(void) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, split_kernel);
+  cudaFuncGetAttributes(&a, split_transpose_kernel);
+  cudaFuncGetAttributes(&a, gemm_tc_kernel);
+  cudaFuncGetAttributes(&a, pair::gemm_tc_pair_kernel);
+  cudaFuncGetAttributes(&a, pair::zero_tiles_kernel);
+  cudaFuncGetAttributes(&a, pair::prep_kernel);
+  cudaGetLastError();
+}

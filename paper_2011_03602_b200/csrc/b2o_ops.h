@@ -15,6 +15,12 @@ void b2o_cpu_fft2d(const void *x, void *y, int64_t n, int elem);
 // host: h[d[i]] += 1 for i < n (values outside [0, bins) skipped), h of b2o_elem elem
 void b2o_cpu_histogram(const int32_t *d, int64_t n, void *h, int64_t bins, int elem);
 
+// force-load each file's kernels on the current device (b2o_init)
+void b2o_ops_warm(void);
+void b2o_gemm_tc_warm(void);
+void b2o_gemm_warm(void);
+void b2o_xsum_warm(void);
+
 #ifdef __cplusplus
 }
 #endif

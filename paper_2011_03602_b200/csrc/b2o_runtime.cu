@@ -667,6 +667,14 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
   ex.red_exact = cb_red_exact;
   for (int slot = 0; slot < info->exact_slots && info->exact_elems > 0; ++slot)
     if (!red_reserve(d.get(), slot, info->exact_elems)) return fail("exact reduction buffers");
+  if (info->exact_slots > 0) {
+    // load the exact-sum kernels now (lazy module loading would otherwise
+    // charge the first timed pattern for it)
+    if (!red_reserve(d.get(), 0, std::max<int64_t>(info->exact_elems, 1)) ||
+        b2o_exact_sum_f32_ws((const float *)d->red_bufs[0], 1, 0.f, (float *)d->slab, d->xsum_ws, w->stream) != 0 ||
+        cudaStreamSynchronize(w->stream) != cudaSuccess)
+      return fail("exact-sum warm-up");
+  }
   d->pend.assign(nv, AppDev::Pending{});
   d->async_d2h = getenv("B2O_SYNC_D2H") == nullptr;
   ex.pre_launch = cb_pre_launch;
@@ -1018,6 +1026,10 @@ int b2o_init(const int32_t *device_ids, int32_t n) {
       g_rt = nullptr;
       return fail("stream creation on device %d", ids[i]);
     }
+    b2o_ops_warm();
+    b2o_gemm_tc_warm();
+    b2o_gemm_warm();
+    b2o_xsum_warm();
     g_rt->workers.push_back(std::move(w));
   }
   for (auto &w : g_rt->workers) w->th = std::thread(worker_loop, w.get());

@@ -477,3 +477,14 @@ extern "C" int b2o_exact_sum_f32(const float *x, int64_t n, float s0, float *s_o
   }
   return b2o_exact_sum_f32_ws(x, n, s0, s_out, ws, stream);
 }
+
+// force-load this file's kernels (lazy module loading would otherwise charge
+// the first timed pattern that uses one); called per device by b2o_init
+extern "C" void b2o_xsum_warm(void) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, xs_stats_kernel);
+  cudaFuncGetAttributes(&a, xs_window_kernel);
+  cudaFuncGetAttributes(&a, xs_summ_kernel);
+  cudaFuncGetAttributes(&a, xs_compose_kernel);
+  cudaGetLastError();
+}
