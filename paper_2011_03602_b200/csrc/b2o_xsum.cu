@@ -54,90 +54,153 @@ constexpr int XS_PER_LANE = XS_CHUNK / 32;
 constexpr int XS_SUPER = 32;         // chunks per super-chunk (one CTA of 32 warps)
 constexpr int XS_W = 4;              // binades in each super-chunk's window
 
-// A run's effect for one binade, in units u.  Valid summaries have |P|, |lo|,
-// |hi| <= 2^24 + 1 (the running integer stays in [2^23, 2^24)); anything
-// larger is flagged, which also keeps every int32 sum below overflow.
+// A run's effect for one binade, in units u, for both parities of the
+// running integer S at the run's start (variant p: S odd iff p = 1): a term
+// exactly half-way between two multiples of u rounds to the even neighbour,
+// so its increment depends on the parity of S there -- and after it S is
+// even, whichever way it went.  Tracking both start parities keeps ties on
+// the fast path; merging runs maps each start parity through the first run's
+// end parity.  Valid summaries have |P|, |lo|, |hi| <= 2^24 + 1 (the running
+// integer stays in [2^23, 2^24)); larger ones are flagged, which also keeps
+// every int32 sum below overflow.
 struct Summ {
-  int P;      // sum of r
-  int lo;     // min over j of (P_(j+1) - 1)
-  int hi;     // max over j of (P_(j+1) + 1)
-  int flags;  // nonzero: unusable for this binade
+  int P0, P1;    // sum of the increments
+  int lo0, lo1;  // min over j of (P_(j+1) - 1)
+  int hi0, hi1;  // max over j of (P_(j+1) + 1)
+  int flags;     // nonzero: unusable for this binade
+  int pad;
 };
 
 constexpr int kLoEmpty = 0x7FFFFFFF, kHiEmpty = -0x7FFFFFFF - 1;
 constexpr int kBig = 1 << 25;
 
-// r = round(x / 2^(e-23)) with the tie / range flag; x as raw bits.
-// Branch-free (the 16 lanes of a half-warp evaluate 16 different binades).
-// |x| >= 2^(e+1) (d > 0) can never keep the sum inside the binade: flagged.
-__device__ __forceinline__ int units(uint32_t bits, int e, int &flag) {
+// x / 2^(e-23) rounded to nearest, as raw bits: returns round(X) (tie = 0) or
+// floor(X) for a half-way X (tie = 1; the increment is floor(X) + the parity
+// of S + floor(X)).  Branch-free (the lanes of a warp evaluate different
+// binades).  |x| >= 2^(e+1) (d > 0) can never keep the sum in the binade and
+// inf / nan are flagged.
+__device__ __forceinline__ int units(uint32_t bits, int e, int &tie, int &flag) {
   const uint32_t exr = (bits >> 23) & 0xFFu;
   const uint32_t m = (bits & 0x7FFFFFu) | (exr ? 0x800000u : 0u);
   const int ex = exr ? (int)exr - 127 : -126;
   const int d = ex - e;
   const int sh = min(max(-d, 1), 31);
   const uint32_t q = m >> sh, rem = m & ((1u << sh) - 1u), half = 1u << (sh - 1);
-  const int dn = (int)q + (rem > half ? 1 : 0);
-  // round half to even would be decided by S's parity: flag the tie
-  flag |= (exr == 0xFFu) | (d > 0) | (d < 0 && rem == half);
-  const int r = d == 0 ? (int)m : (d < 0 ? dn : 0);
-  return (bits >> 31) ? -r : r;
+  flag |= (exr == 0xFFu) | (d > 0);
+  const bool neg = (bits >> 31) != 0;
+  tie = (d < 0 && rem == half) ? 1 : 0;
+  if (tie) return neg ? -(int)q - 1 : (int)q;  // floor(X)
+  const int r = d == 0 ? (int)m : (d < 0 ? (int)q + (rem > half ? 1 : 0) : 0);
+  return neg ? -r : r;
 }
+
+// apply one term (c, tie) to both variants
+__device__ __forceinline__ void step(Summ &s, int c, int tie) {
+  const int r0 = c + (tie & (s.P0 + c)), r1 = c + (tie & (1 + s.P1 + c));
+  s.P0 += r0;
+  s.P1 += r1;
+  s.lo0 = min(s.lo0, s.P0 - 1);
+  s.hi0 = max(s.hi0, s.P0 + 1);
+  s.lo1 = min(s.lo1, s.P1 - 1);
+  s.hi1 = max(s.hi1, s.P1 + 1);
+}
+
+__device__ __forceinline__ bool out_of_range(int v) { return v > kBig || v < -kBig; }
 
 __device__ __forceinline__ bool big(const Summ &a) {
-  return a.P > kBig || a.P < -kBig || (a.lo != kLoEmpty && (a.lo > kBig || a.lo < -kBig)) ||
-         (a.hi != kHiEmpty && (a.hi > kBig || a.hi < -kBig));
+  return out_of_range(a.P0) || out_of_range(a.P1) || out_of_range(a.lo0) || out_of_range(a.lo1) ||
+         out_of_range(a.hi0) || out_of_range(a.hi1);
 }
 
-// a then b
+#define kEmpty (Summ{0, 0, kLoEmpty, kLoEmpty, kHiEmpty, kHiEmpty, 0, 0})
+#define kInvalid (Summ{0, 0, 0, 0, 0, 0, 1, 0})
+
+// a then b: variant p of a ends with parity (p + a.P_p) & 1, which selects b's
 __device__ __forceinline__ Summ merge(const Summ &a, const Summ &b) {
-  if (b.lo == kLoEmpty) return a;
-  if (a.lo == kLoEmpty) return b;
-  if (a.flags | b.flags || big(a) || big(b)) return Summ{0, 0, 0, 1};
-  return Summ{a.P + b.P, min(a.lo, a.P + b.lo), max(a.hi, a.P + b.hi), 0};
+  if (b.lo0 == kLoEmpty) return a;
+  if (a.lo0 == kLoEmpty) return b;
+  if (a.flags | b.flags || big(a) || big(b)) return kInvalid;
+  const bool x0 = (a.P0 & 1) != 0, x1 = ((1 + a.P1) & 1) != 0;
+  const int bP0 = x0 ? b.P1 : b.P0, bl0 = x0 ? b.lo1 : b.lo0, bh0 = x0 ? b.hi1 : b.hi0;
+  const int bP1 = x1 ? b.P1 : b.P0, bl1 = x1 ? b.lo1 : b.lo0, bh1 = x1 ? b.hi1 : b.hi0;
+  return Summ{a.P0 + bP0, a.P1 + bP1, min(a.lo0, a.P0 + bl0), min(a.lo1, a.P1 + bl1),
+              max(a.hi0, a.P0 + bh0), max(a.hi1, a.P1 + bh1), 0, 0};
 }
 
-// A: per super-chunk sum and sum of magnitudes (double)
+__device__ __forceinline__ Summ shfl_down_summ(const Summ &s, int d) {
+  return Summ{__shfl_down_sync(0xffffffffu, s.P0, d), __shfl_down_sync(0xffffffffu, s.P1, d),
+              __shfl_down_sync(0xffffffffu, s.lo0, d), __shfl_down_sync(0xffffffffu, s.lo1, d),
+              __shfl_down_sync(0xffffffffu, s.hi0, d), __shfl_down_sync(0xffffffffu, s.hi1, d),
+              __shfl_down_sync(0xffffffffu, s.flags, d), 0};
+}
+
+__device__ __forceinline__ Summ shfl_up_summ(const Summ &s, int d) {
+  return Summ{__shfl_up_sync(0xffffffffu, s.P0, d), __shfl_up_sync(0xffffffffu, s.P1, d),
+              __shfl_up_sync(0xffffffffu, s.lo0, d), __shfl_up_sync(0xffffffffu, s.lo1, d),
+              __shfl_up_sync(0xffffffffu, s.hi0, d), __shfl_up_sync(0xffffffffu, s.hi1, d),
+              __shfl_up_sync(0xffffffffu, s.flags, d), 0};
+}
+
+__device__ __forceinline__ Summ shfl_summ(const Summ &s, int src) {
+  return Summ{__shfl_sync(0xffffffffu, s.P0, src), __shfl_sync(0xffffffffu, s.P1, src),
+              __shfl_sync(0xffffffffu, s.lo0, src), __shfl_sync(0xffffffffu, s.lo1, src),
+              __shfl_sync(0xffffffffu, s.hi0, src), __shfl_sync(0xffffffffu, s.hi1, src),
+              __shfl_sync(0xffffffffu, s.flags, src), 0};
+}
+
+// A: per super-chunk (double): its sum, and how far the running sum can get
+// from the super-chunk's starting value: the extreme prefix sums at chunk
+// boundaries plus the largest chunk magnitude (a chunk's own excursion)
 __global__ void __launch_bounds__(256) xs_stats_kernel(const float *__restrict__ x, int64_t n,
-                                                        double *__restrict__ ssum, double *__restrict__ sabs) {
+                                                        double *__restrict__ ssum, double *__restrict__ sreach) {
+  __shared__ double cs[XS_SUPER], ca[XS_SUPER];
   const int64_t b0 = (int64_t)blockIdx.x * XS_SUPER * XS_CHUNK;
-  double a = 0.0, m = 0.0;
-  for (int i = threadIdx.x; i < XS_SUPER * XS_CHUNK; i += blockDim.x) {
-    if (b0 + i < n) {
-      const double v = (double)x[b0 + i];
-      a += v;
-      m += fabs(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < XS_SUPER; c += blockDim.x / 32) {
+    double a = 0.0, m = 0.0;
+    for (int i = lane; i < XS_CHUNK; i += 32) {
+      const int64_t g = b0 + (int64_t)c * XS_CHUNK + i;
+      if (g < n) {
+        const double v = (double)x[g];
+        a += v;
+        m += fabs(v);
+      }
     }
-  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    m += __shfl_xor_sync(0xffffffffu, m, o);
-  }
-  __shared__ double sa[8], sm[8];
-  if ((threadIdx.x & 31) == 0) {
-    sa[threadIdx.x >> 5] = a;
-    sm[threadIdx.x >> 5] = m;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      m += __shfl_xor_sync(0xffffffffu, m, o);
+    }
+    if (lane == 0) {
+      cs[c] = a;
+      ca[c] = m;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double ta = 0.0, tm = 0.0;
-    for (int w = 0; w < 8; ++w) {
-      ta += sa[w];
-      tm += sm[w];
+    double pre = 0.0, lo = 0.0, hi = 0.0, am = 0.0;
+    for (int c = 0; c < XS_SUPER; ++c) {
+      pre += cs[c];
+      lo = fmin(lo, pre);
+      hi = fmax(hi, pre);
+      am = fmax(am, ca[c]);
     }
-    ssum[blockIdx.x] = ta;
-    sabs[blockIdx.x] = tm;
+    ssum[blockIdx.x] = pre;
+    // reach: (lo, hi, chunk magnitude) packed as three doubles
+    sreach[3 * blockIdx.x] = lo;
+    sreach[3 * blockIdx.x + 1] = hi;
+    sreach[3 * blockIdx.x + 2] = am;
   }
 }
 
 // A2: each super-chunk's binade window.  est = s0 + sum of the earlier
-// super-chunks (double); |s| inside the super-chunk is at most |est| + its
-// magnitudes, with 25 % slack for the drift of the fp32 running sum from the
-// exact one; the window is the XS_W binades up to that bound (a running sum
-// below it is added element by element: exact, only slower).
+// super-chunks (double); |s| inside the super-chunk is at most
+// max(|est + lo|, |est + hi|) + the largest chunk magnitude, with 25 % slack
+// for the drift of the fp32 running sum from the exact one; the window is the
+// XS_W binades up to that bound (a running sum below it is added element by
+// element: exact, only slower).
 __global__ void __launch_bounds__(1024) xs_window_kernel(const double *__restrict__ ssum,
-                                                          const double *__restrict__ sabs, int64_t nsupers,
+                                                          const double *__restrict__ sreach, int64_t nsupers,
                                                           float s0, int *__restrict__ ebase) {
   __shared__ double part[1024];
   const int t = threadIdx.x;
@@ -155,7 +218,8 @@ __global__ void __launch_bounds__(1024) xs_window_kernel(const double *__restric
   }
   double est = (double)s0 + (t > 0 ? part[t - 1] : 0.0);
   for (int64_t i = i0; i < i1; ++i) {
-    const double top = (fabs(est) + sabs[i]) * 1.25 + 1e-30;
+    const double reach = fmax(fabs(est + sreach[3 * i]), fabs(est + sreach[3 * i + 1])) + sreach[3 * i + 2];
+    const double top = reach * 1.25 + 1e-30;
     int e;
     frexp(top, &e);  // top in [2^(e-1), 2^e)
     ebase[i] = (e - 1) - (XS_W - 1);
@@ -185,9 +249,11 @@ __global__ void __launch_bounds__(1024) xs_summ_kernel(const float *__restrict__
   const int k = lane & (XS_W - 1), part = lane >> 2;
   const int e = ebase[blockIdx.x] + k;
   constexpr int PART = XS_CHUNK / 8;
-  int P = 0, lo = kLoEmpty, hi = kHiEmpty, flag = 0;
+  Summ s = kEmpty;
+  int flag = 0;
   const int i0 = part * PART, i1 = min(i0 + PART, cnt);
   const float *row = &xs[warp][part * (PART + 1)];
+  if (i1 > i0) s = Summ{0, 0, kLoEmpty, kLoEmpty, kHiEmpty, kHiEmpty, 0, 0};
   if (i1 - i0 == PART) {
 #pragma unroll 4
     for (int i = 0; i < PART; i += 8) {
@@ -196,23 +262,22 @@ __global__ void __launch_bounds__(1024) xs_summ_kernel(const float *__restrict__
       for (int j = 0; j < 8; ++j) b[j] = __float_as_uint(row[i + j]);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        P += units(b[j], e, flag);  // |P| < 32 * 2^24: no overflow
-        lo = min(lo, P - 1);
-        hi = max(hi, P + 1);
+        int tie;
+        const int c = units(b[j], e, tie, flag);  // |P| < 32 * 2^24: no overflow
+        step(s, c, tie);
       }
     }
   } else {
     for (int i = 0; i < i1 - i0; ++i) {
-      P += units(__float_as_uint(row[i]), e, flag);
-      lo = min(lo, P - 1);
-      hi = max(hi, P + 1);
+      int tie;
+      const int c = units(__float_as_uint(row[i]), e, tie, flag);
+      step(s, c, tie);
     }
   }
-  Summ s{P, lo, hi, flag};
+  s.flags = flag;
 #pragma unroll
   for (int d = 4; d < 32; d <<= 1) {  // ordered merge: part p with part p + d/4
-    Summ t{__shfl_down_sync(0xffffffffu, s.P, d), __shfl_down_sync(0xffffffffu, s.lo, d),
-           __shfl_down_sync(0xffffffffu, s.hi, d), __shfl_down_sync(0xffffffffu, s.flags, d)};
+    const Summ t = shfl_down_summ(s, d);
     if ((part & (2 * (d >> 2) - 1)) == 0) s = merge(s, t);
   }
   if (lane < XS_W) {
@@ -244,22 +309,24 @@ __device__ __forceinline__ WalkState state_of(float s) {
                    (bits >> 31) != 0};
 }
 
-#define kEmpty (Summ{0, kLoEmpty, kHiEmpty, 0})
-#define kInvalid (Summ{0, 0, 0, 1})
-
-// a run summary (for s's binade) is usable from state w.  s < 0 runs the
-// mirrored problem: fl(s + x) = -fl(|s| + (-x)), whose units are -r, so the
-// prefix range flips (|S| - hi, |S| - lo) and S' = |S| - P.
+// a run summary (for s's binade) is usable from state w: the variant of S's
+// parity.  s < 0 runs the mirrored problem fl(s + x) = -fl(|s| + (-x)): the
+// increments negate (ties included, round-half-even being symmetric) and the
+// parity evolution is the same, so the prefix range flips (|S| - hi,
+// |S| - lo) and S' = |S| - P.
 __device__ __forceinline__ bool usable(const Summ &t, const WalkState &w) {
   if (t.flags) return false;
-  if (t.lo == kLoEmpty) return true;
-  return w.neg ? (w.S - t.hi >= (1 << 23) && w.S - t.lo <= (1 << 24))
-               : (w.S + t.lo >= (1 << 23) && w.S + t.hi <= (1 << 24));
+  if (t.lo0 == kLoEmpty) return true;
+  const bool odd = (w.S & 1) != 0;
+  const int lo = odd ? t.lo1 : t.lo0, hi = odd ? t.hi1 : t.hi0;
+  return w.neg ? (w.S - hi >= (1 << 23) && w.S - lo <= (1 << 24))
+               : (w.S + lo >= (1 << 23) && w.S + hi <= (1 << 24));
 }
 
 __device__ __forceinline__ float advance(float s, const Summ &t, const WalkState &w) {
-  if (t.lo == kLoEmpty) return s;
-  const int S2 = w.neg ? w.S - t.P : w.S + t.P;
+  if (t.lo0 == kLoEmpty) return s;
+  const int P = (w.S & 1) ? t.P1 : t.P0;
+  const int S2 = w.neg ? w.S - P : w.S + P;
   return __uint_as_float((__float_as_uint(s) & 0xFF800000u) | (uint32_t)(S2 - (1 << 23)));
 }
 
@@ -271,17 +338,12 @@ __device__ __forceinline__ int scan_apply(float &s, Summ mine, int first, int cn
   Summ pre = mine;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const Summ t{__shfl_up_sync(0xffffffffu, pre.P, d), __shfl_up_sync(0xffffffffu, pre.lo, d),
-                 __shfl_up_sync(0xffffffffu, pre.hi, d), __shfl_up_sync(0xffffffffu, pre.flags, d)};
+    const Summ t = shfl_up_summ(pre, d);
     if (lane >= d) pre = merge(t, pre);
   }
   const unsigned bad = __ballot_sync(0xffffffffu, lane >= first && lane < cnt && !usable(pre, w));
   const int f = bad ? __ffs(bad) - 1 : cnt;
-  if (f > first) {
-    const Summ t{__shfl_sync(0xffffffffu, pre.P, f - 1), __shfl_sync(0xffffffffu, pre.lo, f - 1),
-                 __shfl_sync(0xffffffffu, pre.hi, f - 1), __shfl_sync(0xffffffffu, pre.flags, f - 1)};
-    s = advance(s, t, w);
-  }
+  if (f > first) s = advance(s, shfl_summ(pre, f - 1), w);
   return f - first;
 }
 
@@ -297,26 +359,27 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
                                                          const Summ *__restrict__ chunks,
                                                          const Summ *__restrict__ supers, int64_t nchunks,
                                                          int64_t nsupers, float *out, int stats) {
-  __shared__ int4 sbuf[2][32 * XS_W];
-  __shared__ int4 cbuf[XS_SUPER * XS_W];
+  constexpr int R4 = (int)(sizeof(Summ) / sizeof(int4));  // int4 per record
+  __shared__ int4 sbuf[2][32 * XS_W * R4];
+  __shared__ int4 cbuf[XS_SUPER * XS_W * R4];
   __shared__ __align__(16) float xbuf[XS_CHUNK];
   const int lane = threadIdx.x;
   const int4 *sup4 = reinterpret_cast<const int4 *>(supers);
   const int4 *chk4 = reinterpret_cast<const int4 *>(chunks);
   int n_desc = 0, n_slow = 0;
-  int4 pre[XS_W];
+  int4 pre[XS_W * R4];
   int peb = 0;
   auto fetch = [&](int64_t g) {
 #pragma unroll
-    for (int j = 0; j < XS_W; ++j) {
-      const int64_t r = g * 32 * XS_W + lane + 32 * j;
-      pre[j] = r < nsupers * XS_W ? sup4[r] : make_int4(0, 0, 0, 1);
+    for (int j = 0; j < XS_W * R4; ++j) {
+      const int64_t r = g * 32 * XS_W * R4 + lane + 32 * j;
+      pre[j] = r < nsupers * XS_W * R4 ? sup4[r] : make_int4(0, 0, 0, 0);
     }
     peb = g * 32 + lane < nsupers ? ebase[g * 32 + lane] : 0;
   };
   auto stash = [&](int b) {
 #pragma unroll
-    for (int j = 0; j < XS_W; ++j) sbuf[b][lane + 32 * j] = pre[j];
+    for (int j = 0; j < XS_W * R4; ++j) sbuf[b][lane + 32 * j] = pre[j];
   };
   float s = s0;
   const int64_t ngroups = (nsupers + 31) / 32;
@@ -346,9 +409,9 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
       const int nc = (int)(c1 - c0);
       __syncwarp();
 #pragma unroll
-      for (int j = 0; j < XS_W; ++j) {
-        const int64_t r = c0 * XS_W + lane + 32 * j;
-        cbuf[lane + 32 * j] = r < nchunks * XS_W ? chk4[r] : make_int4(0, 0, 0, 1);
+      for (int j = 0; j < XS_W * R4; ++j) {
+        const int64_t r = c0 * XS_W * R4 + lane + 32 * j;
+        cbuf[lane + 32 * j] = r < nchunks * XS_W * R4 ? chk4[r] : make_int4(0, 0, 0, 0);
       }
       __syncwarp();
       const Summ *crec = reinterpret_cast<const Summ *>(cbuf);
@@ -413,7 +476,7 @@ std::map<int, Workspace> ws_by_dev;
 
 struct Layout {
   int64_t nchunks, nsupers;
-  size_t ssum, sabs, ebase, chunks, supers, bytes;
+  size_t ssum, sreach, ebase, chunks, supers, bytes;
 };
 
 Layout layout(int64_t n) {
@@ -422,8 +485,8 @@ Layout layout(int64_t n) {
   L.nsupers = (L.nchunks + XS_SUPER - 1) / XS_SUPER;
   auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
   L.ssum = 0;
-  L.sabs = up(L.ssum + sizeof(double) * L.nsupers);
-  L.ebase = up(L.sabs + sizeof(double) * L.nsupers);
+  L.sreach = up(L.ssum + sizeof(double) * L.nsupers);  // (lo, hi, chunk magnitude) per super-chunk
+  L.ebase = up(L.sreach + 3 * sizeof(double) * L.nsupers);
   L.chunks = up(L.ebase + sizeof(int) * (L.nsupers + 32));
   L.supers = up(L.chunks + sizeof(Summ) * XS_W * L.nchunks);
   L.bytes = up(L.supers + sizeof(Summ) * XS_W * (L.nsupers + 32));
@@ -444,11 +507,11 @@ extern "C" int b2o_exact_sum_f32_ws(const float *x, int64_t n, float s0, float *
   }
   const Layout L = layout(n);
   char *ws = (char *)workspace;
-  double *ssum = (double *)(ws + L.ssum), *sabs = (double *)(ws + L.sabs);
+  double *ssum = (double *)(ws + L.ssum), *sreach = (double *)(ws + L.sreach);
   int *ebase = (int *)(ws + L.ebase);
   Summ *chunks = (Summ *)(ws + L.chunks), *supers = (Summ *)(ws + L.supers);
-  xs_stats_kernel<<<(unsigned)L.nsupers, 256, 0, st>>>(x, n, ssum, sabs);
-  xs_window_kernel<<<1, 1024, 0, st>>>(ssum, sabs, L.nsupers, s0, ebase);
+  xs_stats_kernel<<<(unsigned)L.nsupers, 256, 0, st>>>(x, n, ssum, sreach);
+  xs_window_kernel<<<1, 1024, 0, st>>>(ssum, sreach, L.nsupers, s0, ebase);
   xs_summ_kernel<<<(unsigned)L.nsupers, 1024, 0, st>>>(x, n, ebase, chunks, supers, L.nchunks);
   static const int stats = getenv("B2O_XSUM_STATS") != nullptr;
   xs_compose_kernel<<<1, 32, 0, st>>>(x, n, ebase, s0, chunks, supers, L.nchunks, L.nsupers, s_out, stats);

@@ -16,7 +16,9 @@ L = lib()
 st = torch.cuda.current_stream().cuda_stream
 for name, n, gen in (("uniform", 4_112_895, lambda r, n: r.random(n, dtype=np.float32)),
                      ("squares", 4_112_895, lambda r, n: (r.standard_normal(n, dtype=np.float32) * 1e-3) ** 2),
-                     ("mixed_sign", 4_112_895, lambda r, n: r.standard_normal(n, dtype=np.float32))):
+                     ("mixed_sign", 4_112_895, lambda r, n: r.standard_normal(n, dtype=np.float32)),
+                     ("dyadic", 4_112_895, lambda r, n: (r.integers(0, 64, n) * np.float32(2.0 ** -10)).astype(np.float32)),
+                     ("constant", 4_112_895, lambda r, n: np.full(n, np.float32(0.1)))):
     x = torch.from_numpy(gen(np.random.default_rng(5), n)).cuda()
     out = torch.empty(1, device="cuda")
     for _ in range(3):
