@@ -4,38 +4,42 @@
 //
 // Why it parallelises: while the running sum s stays inside one binade
 // [2^e, 2^(e+1)) it is an integer S in units u = 2^(e-23), S in [2^23, 2^24),
-// and (unless x is exactly half-way between two multiples of u)
+// and
 //
 //     fl(s + x) = (S + r) u,   r = round-to-nearest(x / u),
 //
-// provided the exact sum stays inside the binade.  r depends on x and e only,
-// not on s, so for a fixed binade the effect of a whole run of elements is an
-// integer sum -- associative, hence scan-able -- plus the range of the
-// running integer prefix (to check that s never left the binade).  Every
-// element's validity condition is kept conservative:
+// provided the exact sum stays inside the binade.  r depends on x and e only
+// -- except for an x exactly half-way between two multiples of u, which
+// rounds to the even neighbour: r = floor(x / u) + parity(S + floor(x / u)),
+// after which S is even.  So for a fixed binade the effect of a run of
+// elements is, for each parity of S at its start, an integer sum plus the
+// range of the running integer prefix (to check that s never left the
+// binade); runs compose associatively (the first run's end parity selects
+// the second's variant), hence scan-ably.  Every element's validity
+// condition is kept conservative:
 //
 //     S + P_j + r_j - 1 >= 2^23   and   S + P_j + r_j + 1 <= 2^24
 //
-// (P_j = r_0 + ... + r_(j-1)); a half-way x (a tie: the result would depend
-// on the parity of S), an infinity / NaN, or an x too large for the binade
-// flags the run as unusable.
+// (P_j = r_0 + ... + r_(j-1)); an infinity / NaN or an x too large for the
+// binade flags the run as unusable.
 //
 // Four kernels on the caller's stream:
-//   A  stats:    per super-chunk (8192 terms) sum and sum of magnitudes;
+//   A  stats:    per super-chunk (8192 terms) its sum and its reach (extreme
+//                chunk-boundary prefixes + the largest chunk magnitude);
 //   A2 window:   one CTA scans the sums: each super-chunk gets the 4 binades
-//                below (|s0 + earlier sums| + its magnitudes) * 1.25;
+//                below (|s0 + earlier sums| + its reach) * 1.25;
 //   B  summarise: per chunk of 256 terms (one warp: 8 parts x 4 binades) and
-//                per super-chunk: (P, min prefix - 1, max prefix + 1, flags)
-//                for each window binade;
+//                per super-chunk: (P, min prefix - 1, max prefix + 1) for
+//                both start parities, and flags, for each window binade;
 //   C  compose:  one warp walks the super-chunks 32 at a time: lane i picks
 //                super-chunk i's record for the running sum's binade, a warp
 //                scan merges them in order and the longest usable prefix is
 //                applied in O(1); a super-chunk that is not usable is walked
 //                by its chunks the same way, and a chunk that is not usable
-//                either (a binade crossing, a tie, a running sum outside the
-//                window or not normal) is added element by element with
-//                __fadd_rn -- the definition itself.
-// Himeno M's 4.1 M gosa terms: 0.17 ms (15 descents, 23 element-wise chunks).
+//                either (a binade crossing, a running sum outside the window
+//                or not normal) is added element by element with __fadd_rn --
+//                the definition itself.
+// Himeno M's 4.1 M gosa terms: 0.15 ms (10 descents, 16 element-wise chunks).
 #include <cuda_runtime.h>
 
 #include <cmath>
