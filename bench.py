@@ -187,6 +187,16 @@ def ncu_traffic(kernel: str) -> float | None:
 # ---------------------------------------------------------------------------
 
 
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_run(doc: dict, spec: dict, openmp: bool, runs: int) -> tuple[float, int]:
     from oracle.cgen import CProgram
     from paper_2011_03602_b200 import appspec
@@ -280,6 +290,8 @@ def b200_arm(args, dist: Dist) -> None:
     # the CPU baseline is timed on rank 0 at N=1 only (other ranks would
     # contend for the same host cores)
     cpu_s, cores = cpu_run(g["doc"], g["spec"], openmp=True, runs=1) if dist.world == 1 else (None, None)
+    # the faithful sequential semantics too (both reported)
+    cpu1_s, _ = cpu_run(g["doc"], g["spec"], openmp=False, runs=1) if dist.world == 1 else (None, None)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
@@ -301,6 +313,9 @@ def b200_arm(args, dist: Dist) -> None:
                          "kind": "port", "sample": f"one full Himeno M app run ({nn} sweeps), C restatement "
                                                    "(oracle/cgen.py), gcc -O3 OpenMP, all-CPU genome"}
         if cpu_s else None,
+        "cpu_baseline_1core": {"value": round(bytes_per_step / cpu1_s / 1e9, 3), "unit": "GB/s", "cores": 1,
+                               "kind": "port", "sample": "the same app run, single-threaded (sequential C semantics)",
+                               "cpu_model": cpu_model()} if cpu1_s else None,
         "app_speedup_vs_cpu": round(cpu_s / e2e_s, 2) if cpu_s else None,
         "ga": ga,
         "ops": ops,
