@@ -241,7 +241,7 @@ def reference_arm(args, dist: Dist) -> None:
                    "sweeps": nn},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "port",
                          "sample": f"one full Himeno M app run ({nn} sweeps) per step, C restatement (oracle/cgen.py) "
-                                   f"gcc -O3 OpenMP"},
+                                   f"gcc -O3 OpenMP", "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -311,7 +311,8 @@ def b200_arm(args, dist: Dist) -> None:
         "kernels_us": {f"b2o_k{k}": round(v * 1e3, 2) for k, v in rep["kernel_ms"].items()},
         "cpu_baseline": {"value": round(bytes_per_step / cpu_s / 1e9, 3), "unit": "GB/s", "cores": cores,
                          "kind": "port", "sample": f"one full Himeno M app run ({nn} sweeps), C restatement "
-                                                   "(oracle/cgen.py), gcc -O3 OpenMP, all-CPU genome"}
+                                                   "(oracle/cgen.py), gcc -O3 OpenMP, all-CPU genome",
+                         "cpu_model": cpu_model()}
         if cpu_s else None,
         "cpu_baseline_1core": {"value": round(bytes_per_step / cpu1_s / 1e9, 3), "unit": "GB/s", "cores": 1,
                                "kind": "port", "sample": "the same app run, single-threaded (sequential C semantics)",
