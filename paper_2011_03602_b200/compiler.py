@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-28"
+COMPILER_VERSION = "b2o-compiler-30"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -1007,8 +1007,10 @@ class _Gen:
         for v in n.scalar_args:
             out.append(f"  a.s{v} = S{v};")
         if n.shape == "ktile":
-            out.append(f"  geom[0] = (a.n[1] + {KT_TJ - 1}) / {KT_TJ}; geom[1] = (a.n[0] + {KT_TI - 1}) / {KT_TI}; "
-                       f"geom[2] = 1; geom[3] = {KT_TI * KT_TJ // (KT_R * KT_R)}; geom[4] = geom[5] = 1;")
+            T = int(self.spec.get("ktile_tile", KT_TI))
+            R = int(self.spec.get("ktile_r", KT_R))
+            out.append(f"  geom[0] = (a.n[1] + {T - 1}) / {T}; geom[1] = (a.n[0] + {T - 1}) / {T}; "
+                       f"geom[2] = 1; geom[3] = {T * T // (R * R)}; geom[4] = geom[5] = 1;")
         elif n.shape == "brick":
             tk, tj = STENCIL_TILE
             out.append(f"  geom[0] = (a.n[2] + {tk - 1}) / {tk}; geom[1] = (a.n[1] + {tj - 1}) / {tj}; "
@@ -1551,7 +1553,8 @@ class _Gen:
         lid = n.root
         kp = n.ktile
         iv, jv, kv = kp["iv"], kp["jv"], kp["kv"]
-        R, TI, TJ, BK = KT_R, KT_TI, KT_TJ, KT_BK
+        T = int(self.spec.get("ktile_tile", KT_TI))
+        R, TI, TJ, BK = int(self.spec.get("ktile_r", KT_R)), T, T, KT_BK
         nthr = TI * TJ // (R * R)
         TX = TJ // R  # threads along j
         K = prog.loops[kp["kloop"]]
@@ -1684,9 +1687,10 @@ class _Gen:
         out.append("      const int32_t vK_ = kb_ + kk_;")
         for (v, co, c0), (side, t) in tiles:
             nm, off = (f"a{t}", "ty_") if side == "A" else (f"b{t}", "tx_")
-            out.append(f"      const float4 {nm}q_ = *reinterpret_cast<const float4 *>(&s{t}_[kk_][{off} * {R}]);")
+            for h_ in range(R // 4):
+                out.append(f"      const float4 {nm}q{h_}_ = *reinterpret_cast<const float4 *>(&s{t}_[kk_][{off} * {R} + {4 * h_}]);")
             for p_ in range(R):
-                out.append(f"      const float {nm}_{p_} = {nm}q_.{'xyzw'[p_]};")
+                out.append(f"      const float {nm}_{p_} = {nm}q{p_ // 4}_.{'xyzw'[p_ % 4]};")
         emit(kbody, True, "      ")
         out.append("      (void)vK_;")
         out.append("    }")
@@ -2096,7 +2100,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "progressive_d2h", "exact_reductions", "reductions")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "progressive_d2h", "exact_reductions", "ktile_tile", "ktile_r", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

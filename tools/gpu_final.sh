@@ -1,0 +1,11 @@
+# Round-end evidence: GPU tests, smoke, bench (both arms), launch list of the
+# bench command, one ncu --set full capture of the dominant kernel.
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > gpurun_out/gpu.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 3 --warmup 3 --ga 0 --ops 0 --reductions 0 > gpurun_out/ncu_launches.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:b2o_k1 -s 4 -c 1 -o gpurun_out/jacobi_final python bench.py --steps 3 --warmup 3 --ga 0 --ops 0 --reductions 0 > gpurun_out/ncu_jacobi.log 2>&1
