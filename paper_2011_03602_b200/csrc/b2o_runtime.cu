@@ -41,6 +41,7 @@
 #include "../../include/b2o.h"
 #include "b2o_module.h"
 #include "b2o_ops.h"
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges for ncu --nvtx / nsys
 
 namespace {
 
@@ -871,14 +872,18 @@ void execute(Worker *w, Job &j) {
   double reset_ms = 0.0;
   for (int rep = 0; rep < reps; ++rep) {
     auto tr = Clock::now();
+    nvtxRangePushA("b2o:reset");
     reset_state(d);
+    nvtxRangePop();
     reset_ms += std::chrono::duration<double, std::milli>(Clock::now() - tr).count();
     w->timed_out = 0;
     w->deadline_ns = j.pat.timeout_s > 0 ? now_ns() + (int64_t)(j.pat.timeout_s * 1e9) : 0;
     w->running = &d->ex;
     auto t0 = Clock::now();
+    nvtxRangePushA("b2o:pattern");  // the timed program run
     j.app->run(&d->ex);
     cudaError_t e = cudaStreamSynchronize(w->stream);
+    nvtxRangePop();
     wait_host_all(d);  // downloads no CPU loop waited for are complete with the stream
     auto t1 = Clock::now();
     w->running = nullptr;
@@ -921,7 +926,9 @@ void execute(Worker *w, Job &j) {
     return;
   }
   auto tc = Clock::now();
+  nvtxRangePushA("b2o:compare");
   compare_outputs(d, r);
+  nvtxRangePop();
   d->have_final = true;
   if (trace) {
     auto te = Clock::now();
