@@ -55,3 +55,29 @@ def test_module_abi_matches(tmp_path):
 def test_init_without_gpu_fails_loudly():
     with pytest.raises(runtime.B2OError):
         runtime.Runtime([0])
+
+
+def _build_c_consumer():
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None or not (ROOT / "paper_2011_03602_b200" / "libb2o.so").exists():
+        pytest.skip("gcc or libb2o.so missing")
+    subprocess.run(["make", "-s", "-B", "-C", str(ROOT / "tests" / "c")], check=True, capture_output=True, text=True)
+    return ROOT / "tests" / "c" / "abi_ops"
+
+
+def test_c_consumer_builds_against_the_header():
+    """A plain-C program (tests/c/abi_ops.c) compiles against include/b2o.h
+    and links libb2o.so: the boundary needs neither Python nor torch."""
+    assert _build_c_consumer().exists()
+
+
+@pytest.mark.gpu
+def test_c_consumer_runs():
+    import subprocess
+
+    exe = _build_c_consumer()
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
+    assert "bit-exact" in r.stdout and "histogram: exact" in r.stdout
