@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
@@ -723,7 +724,7 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
     if (!make_map(&mAh, Ah, (int)m, (int)k, pair::BM) || !make_map(&mAl, Al, (int)m, (int)k, pair::BM) ||
         !make_map(&mBh, Bh, (int)n, (int)k, pair::BNH) || !make_map(&mBl, Bl, (int)n, (int)k, pair::BNH))
       return -1;
-    static bool pattr[64] = {false};
+    static std::atomic<bool> pattr[64];  // per device; set once, racing setters are idempotent
     if (!pattr[dev & 63]) {
       if (cudaFuncSetAttribute(pair::gemm_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                pair::SMEM_BYTES) != cudaSuccess)
@@ -771,7 +772,7 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
   if (!make_map(&mAh, Ah, (int)m, (int)k, BM) || !make_map(&mAl, Al, (int)m, (int)k, BM) ||
       !make_map(&mBh, Bh, (int)n, (int)k, BN) || !make_map(&mBl, Bl, (int)n, (int)k, BN))
     return -1;
-  static bool attr[64] = {false};
+  static std::atomic<bool> attr[64];
   if (!attr[dev & 63]) {
     if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
       return -1;

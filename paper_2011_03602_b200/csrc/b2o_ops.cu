@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <complex>
@@ -596,7 +597,7 @@ extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) 
     float2 *tw = twiddles(n, true);
     if (!tw) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-    static bool attr16[64] = {false};
+    static std::atomic<bool> attr16[64];
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr16[dev & 63]) {
@@ -607,7 +608,7 @@ extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) 
     if (n == 4096 && !getenv("B2O_FFT_LEGACY")) {
       fft4k_rows_kernel<<<4096, 256, 0, s>>>((const float2 *)x, (float2 *)y, tw);
       // cluster of 16 CTAs (non-portable size) when the device takes it, else 8 x 2 sub-FFTs
-      static int npc[64] = {0};
+      static std::atomic<int> npc[64];
       if (npc[dev & 63] == 0 && getenv("B2O_FFT_NPC")) npc[dev & 63] = atoi(getenv("B2O_FFT_NPC"));
       if (npc[dev & 63] == 0) {
         cudaError_t e = launch_cols_cluster<1>((float2 *)y, tw, s);
@@ -640,7 +641,7 @@ extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) 
   cudaStream_t s = (cudaStream_t)stream;
   size_t row_smem = sizeof(float2) * n;
   size_t col_smem = sizeof(float2) * n * kColGroup;
-  static bool attr_set[64] = {false};
+  static std::atomic<bool> attr_set[64];
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
