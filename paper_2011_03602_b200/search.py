@@ -235,6 +235,7 @@ class ShardedEvaluator:
         self.concurrency_safe = True
         self.needs_code = getattr(inner, "needs_code", True)
         self.parallel_width = self.world * max(1, int(getattr(inner, "parallel_width", 1)))
+        self._runs: dict = {}  # run key -> gathered (time, validity, evaluator, diagnostics)
 
     def measure(self, request):
         return self.measure_batch([request])[0]
@@ -256,8 +257,6 @@ class ShardedEvaluator:
         if keys is None:
             todo = list(range(len(requests)))
         else:
-            if not hasattr(self, "_runs"):
-                self._runs: dict = {}
             firsts: dict = {}
             for i, k in enumerate(keys):
                 if k not in self._runs and k not in firsts:
