@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-30"
+COMPILER_VERSION = "b2o-compiler-31"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -1617,8 +1617,9 @@ class _Gen:
             for p_ in range(R):
                 for q_ in range(R):
                     if first_read.get(v):
-                        idx = sub(("arr", v, self._acc_index(kp, v)), p_, q_, False)
-                        out.append(f"  float acc{v}_{p_}{q_} = (vI{p_} < ie_ && vJ{q_} < je_) ? {idx} : 0.f;")
+                        # the accumulator starts from the array's current value
+                        idx = sub(self._acc_index(kp, v), p_, q_, False)
+                        out.append(f"  float acc{v}_{p_}{q_} = (vI{p_} < ie_ && vJ{q_} < je_) ? v{v}[{idx}] : 0.f;")
                     else:
                         out.append(f"  float acc{v}_{p_}{q_} = 0.f;")
 

@@ -23,7 +23,7 @@ from __future__ import annotations
 
 import random
 
-SEEDS = list(range(18))  # 6 per family
+SEEDS = list(range(36))  # 12 per family
 
 
 def family(seed: int) -> str:
