@@ -23,11 +23,13 @@ from __future__ import annotations
 
 import random
 
-SEEDS = list(range(36))  # 12 per family
+SEEDS = list(range(54))  # 12 per original family, 6 per second-generation family
 
 
 def family(seed: int) -> str:
-    return ("ktile", "march", "reduce")[seed % 3]
+    if seed < 36:
+        return ("ktile", "march", "reduce")[seed % 3]
+    return ("ktile2", "march2", "reduce2")[seed % 3]
 
 
 def _ktile(rng: random.Random) -> str:
@@ -111,19 +113,88 @@ def _reduce(rng: random.Random) -> str:
     return "\n".join(lines) + "\n\nfunc main() {\n" + inner + "\n  chk = s0 + s1 + d[7];\n}\n"
 
 
+def _ktile2(rng: random.Random) -> str:
+    """Several k-loop statements: two updates of one accumulator, a second
+    accumulator, constant operand offsets."""
+    ni, nj, nk = rng.choice([40, 64, 72]), rng.choice([24, 64, 66]), rng.choice([8, 33, 48])
+    a = rng.choice([f"a[i * {nk} + k]", f"a[k * {ni} + i + 1]"])
+    b = rng.choice([f"b[k * {nj} + j]", f"b[j * {nk} + k + 2]"])
+    c, e = f"c[i * {nj} + j]", f"e[i * {nj} + j]"
+    body = [f"{c} = {c} + {a} * {b};"]
+    body.append(rng.choice([f"{c} = {c} - {a} * w;", f"{e} = {e} + {b};", f"{e} = {e} * w + {a};"]))
+    if rng.random() < 0.5:
+        body.append(f"{c} = {c} * 0.5 + {b};")
+    init = rng.choice(["", f"{c} = 1.0;\n        {e} = 0.0;", f"{e} = d[i * {nj} + j];"])
+    n = (max(ni, nj, nk) + 4) ** 2
+    lines = ["int i;", "int j;", "int k;", "float w = 0.625;", "float chk;"] + [f"float {x}[{n}];" for x in "abcde"]
+    nest = (f"    for (i = 0; i < {ni}; i++) {{\n      for (j = 0; j < {nj}; j++) {{\n"
+            + (f"        {init}\n" if init else "")
+            + f"        for (k = 0; k < {nk}; k++) {{\n" + "".join(f"          {x}\n" for x in body) + "        }\n"
+            + "      }\n    }\n")
+    return "\n".join(lines) + "\n\nfunc main() {\n" + nest + f"  chk = c[{nj + 1}] + e[3];\n}}\n"
+
+
+def _march2(rng: random.Random) -> str:
+    """Two statements per point (two outputs from the same neighbours), plane
+    offsets of two arrays."""
+    n = rng.choice([12, 16])
+
+    def ix(d3=0, d2=0, d1=0):
+        def t(name, d):
+            return name if d == 0 else (f"({name} + {d})" if d > 0 else f"({name} - {-d})")
+        return f"({t('i3', d3)} * {n} + {t('i2', d2)}) * {n} + {t('i1', d1)}"
+
+    offs = [(a, b, c) for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)]
+    pu = rng.sample(offs, rng.randint(3, 8)) + [(1, 0, 0)]
+    pv = rng.sample(offs, rng.randint(1, 4))
+    tu = " + ".join(f"u[{ix(*o)}]" for o in pu)
+    tv = " + ".join(f"v[{ix(*o)}]" for o in pv)
+    lines = [f"r[{ix()}] = c1 * ({tu}) - {tv};", f"q[{ix()}] = u[{ix()}] * c0 + v[{ix(1, 0, 0)}];"]
+    rng.shuffle(lines)
+    body = (f"    for (i3 = 1; i3 < {n - 1}; i3++) {{\n      for (i2 = 1; i2 < {n - 1}; i2++) {{\n"
+            f"        for (i1 = 1; i1 < {n - 1}; i1++) {{\n" + "".join(f"          {x}\n" for x in lines)
+            + "        }\n      }\n    }\n")
+    m = n ** 3
+    return ("int i1;\nint i2;\nint i3;\nfloat c0 = 0.5;\nfloat c1 = 1.0 / 6.0;\nfloat chk;\n"
+            f"float u[{m}];\nfloat v[{m}];\nfloat r[{m}];\nfloat q[{m}];\n\nfunc main() {{\n"
+            + body + f"  chk = r[{n * n + n + 1}] + q[{n * n + n + 2}];\n}}\n")
+
+
+def _reduce2(rng: random.Random) -> str:
+    """Two fp32 reductions and an int reduction in one nest."""
+    n = rng.choice([32, 48, 64])
+    lines = ["int i;", "int j;", "int k;", "int cnt;", "float w = 0.5;", "float s0;", "float s1;", "float chk;",
+             f"float a[{n * n * n}];", f"float b[{n * n * n}];", f"int t[{n * n * n}];"]
+    depth = rng.choice([2, 3])
+    idx = ["i", "j", "k"][:depth]
+    flat = f"{idx[0]} * {n} + {idx[1]}" if depth == 2 else f"({idx[0]} * {n} + {idx[1]}) * {n} + {idx[2]}"
+    stmts = [f"s0 = s0 + a[{flat}] * w;", f"s1 = s1 - b[{flat}];", f"cnt = cnt + t[{flat}];"]
+    rng.shuffle(stmts)
+    text = "\n".join("    " + "  " * depth + x for x in stmts)
+    for d in reversed(range(depth)):
+        pad = "    " + "  " * d
+        text = f"{pad}for ({idx[d]} = 0; {idx[d]} < {n}; {idx[d]}++) {{\n{text}\n{pad}}}"
+    return "\n".join(lines) + "\n\nfunc main() {\n" + text + "\n  chk = s0 + s1 + cnt;\n}\n"
+
+
 def program(seed: int) -> str:
     rng = random.Random(1000 + seed)
-    return {"ktile": _ktile, "march": _march, "reduce": _reduce}[family(seed)](rng)
+    return {"ktile": _ktile, "march": _march, "reduce": _reduce, "ktile2": _ktile2, "march2": _march2,
+            "reduce2": _reduce2}[family(seed)](rng)
 
 
 def spec(seed: int) -> dict:
     fam = family(seed)
-    arrays = {"ktile": "abcde", "march": ("u", "v", "r"), "reduce": "abd"}[fam]
+    arrays = {"ktile": "abcde", "march": ("u", "v", "r"), "reduce": "abd", "ktile2": "abcde",
+              "march2": ("u", "v", "r", "q"), "reduce2": ("a", "b", "t")}[fam]
     inputs = {x: {"kind": "uniform", "seed": 7 * seed + i, "lo": -1.0 if i % 2 else 0.0, "hi": 1.0}
               for i, x in enumerate(arrays)}
-    outs = list(arrays) + ["chk"] + (["s0", "s1"] if fam == "reduce" else [])
+    if fam == "reduce2":
+        inputs["t"] = {"kind": "randint", "seed": 7 * seed + 9, "lo": -3, "hi": 4}
+    outs = list(arrays) + ["chk"] + (["s0", "s1"] if fam.startswith("reduce") else []) + \
+        (["cnt"] if fam == "reduce2" else [])
     sp = {"name": f"shapes_{seed}", "precision": "fp32", "inputs": inputs,
           "outputs": {o: {"rel_tol": 1e-5} for o in outs}}
-    if fam == "reduce":
+    if fam.startswith("reduce"):
         sp["reductions"] = True
     return sp
