@@ -607,15 +607,26 @@ __global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ A, 
   if (b < nA + nB) {
     const int t = b - nA;
     const int n0 = (t % nBx) * PREP_T, k0 = (t / nBx) * PREP_T;
-    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-    for (int r = ty; r < PREP_T; r += 4) tile[r][tx] = B[(size_t)(k0 + r) * N + n0 + tx];
+    // 16-byte loads along n and 16-byte stores along k: thread (q, r) moves
+    // columns 4q..4q+3 of row r in, rows 4q..4q+3 of column r out
+    const int q = threadIdx.x & 15, r0 = threadIdx.x >> 4;
+    for (int r = r0; r < PREP_T; r += 16) {
+      const float4 v = *reinterpret_cast<const float4 *>(B + (size_t)(k0 + r) * N + n0 + 4 * q);
+      tile[r][4 * q] = v.x;
+      tile[r][4 * q + 1] = v.y;
+      tile[r][4 * q + 2] = v.z;
+      tile[r][4 * q + 3] = v.w;
+    }
     __syncthreads();
-    for (int r = ty; r < PREP_T; r += 4) {
-      float h, l;
-      split_value(tile[tx][r], mode, h, l);
-      const size_t o = (size_t)(n0 + r) * K + k0 + tx;
-      BhT[o] = h;
-      BlT[o] = l;
+    for (int r = r0; r < PREP_T; r += 16) {
+      float4 h, l;
+      split_value(tile[4 * q][r], mode, h.x, l.x);
+      split_value(tile[4 * q + 1][r], mode, h.y, l.y);
+      split_value(tile[4 * q + 2][r], mode, h.z, l.z);
+      split_value(tile[4 * q + 3][r], mode, h.w, l.w);
+      const size_t o = (size_t)(n0 + r) * K + k0 + 4 * q;
+      *reinterpret_cast<float4 *>(BhT + o) = h;
+      *reinterpret_cast<float4 *>(BlT + o) = l;
     }
     return;
   }
