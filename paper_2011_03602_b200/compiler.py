@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-31"
+COMPILER_VERSION = "b2o-compiler-32"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -1067,6 +1067,12 @@ class _Gen:
         return out
 
     def kernel_fn(self, n: NestPlan) -> list[str]:
+        out = self._kernel_fn(n)
+        assert out[0].rstrip().endswith("{"), out[0]
+        # first statement of every kernel: programmatic-dependent-launch entry
+        return [out[0], "  b2o_pdl_enter();"] + out[1:]
+
+    def _kernel_fn(self, n: NestPlan) -> list[str]:
         if n.shape == "stencil":
             return self.stencil_kernel_fn(n)
         if n.shape == "brick":

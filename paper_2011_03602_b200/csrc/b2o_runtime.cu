@@ -174,6 +174,7 @@ struct DriverApi {
   decltype(&::cuModuleGetFunction) moduleGetFunction = nullptr;
   decltype(&::cuModuleUnload) moduleUnload = nullptr;
   decltype(&::cuLaunchKernel) launchKernel = nullptr;
+  decltype(&::cuLaunchKernelEx) launchKernelEx = nullptr;
   decltype(&::cuGetErrorString) getErrorString = nullptr;
 } drv;
 
@@ -190,7 +191,32 @@ bool load_driver_api() {
   return driver_sym("cuModuleLoadData", &drv.moduleLoadData) &&
          driver_sym("cuModuleGetFunction", &drv.moduleGetFunction) &&
          driver_sym("cuModuleUnload", &drv.moduleUnload) && driver_sym("cuLaunchKernel", &drv.launchKernel) &&
+         driver_sym("cuLaunchKernelEx", &drv.launchKernelEx) &&
          driver_sym("cuGetErrorString", &drv.getErrorString);
+}
+
+// generated kernels on the worker stream: programmatic stream serialisation
+// lets a kernel's launch overlap its predecessor's execution (the kernel's
+// b2o_pdl_enter() waits for the predecessor's completion before any access);
+// B2O_PDL=0 launches them plainly
+CUresult launch_app_kernel(CUfunction f, const uint32_t *geom, CUstream st, void **params) {
+  static const bool pdl = !(getenv("B2O_PDL") && atoi(getenv("B2O_PDL")) == 0);
+  if (!pdl) return drv.launchKernel(f, geom[0], geom[1], geom[2], geom[3], geom[4], geom[5], 0, st, params, nullptr);
+  CUlaunchAttribute at[1];
+  at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  at[0].value.programmaticStreamSerializationAllowed = 1;
+  CUlaunchConfig cfg = {};
+  cfg.gridDimX = geom[0];
+  cfg.gridDimY = geom[1];
+  cfg.gridDimZ = geom[2];
+  cfg.blockDimX = geom[3];
+  cfg.blockDimY = geom[4];
+  cfg.blockDimZ = geom[5];
+  cfg.sharedMemBytes = 0;
+  cfg.hStream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return drv.launchKernelEx(&cfg, f, params, nullptr);
 }
 
 int64_t now_ns() {
@@ -450,8 +476,7 @@ void cb_launch(b2o_exec *ex, int32_t loop, void *args, uint32_t args_bytes, cons
     std::copy(geom, geom + 6, L.geom);
     d->log.push_back(std::move(L));
   }
-  if (!cu_ok(d, drv.launchKernel(d->kfun[loop], geom[0], geom[1], geom[2], geom[3], geom[4], geom[5], 0,
-                               (CUstream)d->w->stream, params, nullptr),
+  if (!cu_ok(d, launch_app_kernel(d->kfun[loop], geom, (CUstream)d->w->stream, params),
              "cuLaunchKernel"))
     return;
   d->acc.launches++;
@@ -1245,8 +1270,7 @@ int b2o_bench_replay(uint64_t app, int32_t worker, const b2o_pattern *pattern, i
   auto replay = [&]() -> bool {
     for (auto &L : d->log) {
       void *params[] = {L.args.data()};
-      if (drv.launchKernel(d->kfun[L.loop], L.geom[0], L.geom[1], L.geom[2], L.geom[3], L.geom[4], L.geom[5], 0,
-                           (CUstream)w->stream, params, nullptr) != CUDA_SUCCESS)
+      if (launch_app_kernel(d->kfun[L.loop], L.geom, (CUstream)w->stream, params) != CUDA_SUCCESS)
         return false;
     }
     return true;
@@ -1278,8 +1302,7 @@ int b2o_bench_replay(uint64_t app, int32_t worker, const b2o_pattern *pattern, i
     auto issue = [&]() {
       for (const AppDev::Launch *L : mine) {
         void *params[] = {(void *)L->args.data()};
-        drv.launchKernel(d->kfun[l], L->geom[0], L->geom[1], L->geom[2], L->geom[3], L->geom[4], L->geom[5], 0,
-                         (CUstream)w->stream, params, nullptr);
+        launch_app_kernel(d->kfun[l], L->geom, (CUstream)w->stream, params);
       }
     };
     issue();
