@@ -273,9 +273,11 @@ def b200_arm(args, dist: Dist) -> None:
             r = ev.measure_payloads(g["doc"], [pat])[0]
             e2e.append((time.perf_counter() - t0, r))
         dist.barrier()
-    red = reductions_arm(args, dist) if args.reductions else None
-    ga = ga_arm(args, dist) if args.ga else None
-    ops = ops_arm(dist) if args.ops else None
+    # the side measurements never cost the headline line: a failure is
+    # reported in its own field
+    red = _guarded(reductions_arm, args, dist) if args.reductions else None
+    ga = _guarded(ga_arm, args, dist) if args.ga else None
+    ops = _guarded(ops_arm, dist) if args.ops else None
     ms = dist.max(rep["ms_per_step"])
     e2e_s = dist.max(statistics.median(t for t, _ in e2e))
     last = e2e[-1][1]
@@ -324,6 +326,16 @@ def b200_arm(args, dist: Dist) -> None:
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
+
+
+def _guarded(fn, *args) -> dict:
+    try:
+        return fn(*args)
+    except Exception as exc:  # noqa: BLE001 -- reported, not raised
+        import traceback
+
+        traceback.print_exc(file=sys.stderr)
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
 
 def reductions_arm(args, dist: Dist) -> dict:
