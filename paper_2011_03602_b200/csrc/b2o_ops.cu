@@ -421,6 +421,9 @@ __global__ void __launch_bounds__(512, 2) fft16_cols_kernel(float2 *__restrict__
 __global__ void __launch_bounds__(256) fft4k_rows_kernel(const float2 *__restrict__ x, float2 *__restrict__ y,
                                                           const float2 *__restrict__ tw) {
   __shared__ float2 s[4096];
+  // the column pass (programmatic dependent launch) may start launching now;
+  // it waits for this grid's completion before reading y
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int t = threadIdx.x;
   const float2 *src = x + (size_t)blockIdx.x * 4096;
   float2 v[16];
@@ -481,6 +484,7 @@ template <int NPC>
 __global__ void __launch_bounds__(256 * NPC) fft4k_cols_cluster_kernel(float2 *__restrict__ y,
                                                                         const float2 *__restrict__ tw) {
   extern __shared__ float2 s[];  // NPC x 4096
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the rows pass has completed and is visible
   cg::cluster_group cl = cg::this_cluster();
   constexpr int CL = 16 / NPC;
   const int c = (int)cl.block_rank();
@@ -555,13 +559,15 @@ cudaError_t launch_cols_cluster(float2 *y, const float2 *tw, cudaStream_t s) {
   cfg.blockDim = dim3(256 * NPC);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = getenv("B2O_PDL") && atoi(getenv("B2O_PDL")) == 0 ? 0 : 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, y, tw);
 }
 
