@@ -441,6 +441,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the set-up above overlapped the operand
+  // preparation's tail; global memory (A/B splits, the zeroed C tiles) only
+  // after it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -588,6 +592,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ A, 
                                                    size_t a4, int mode, int nA, int nBx, int nB, float *__restrict__ C,
                                                    int tiles_m, int first_tile) {
   __shared__ float tile[PREP_T][PREP_T + 1];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the MMA kernel may set up meanwhile
   const int b = blockIdx.x;
   if (b < nA) {
     const float4 *x = reinterpret_cast<const float4 *>(A);
@@ -767,13 +772,15 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
     cfg.blockDim = dim3(pair::THREADS);
     cfg.dynamicSmemBytes = pair::SMEM_BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = getenv("B2O_PDL") && atoi(getenv("B2O_PDL")) == 0 ? 0 : 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, pair::gemm_tc_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k, sc) !=
         cudaSuccess)
       return -1;
