@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-32"
+COMPILER_VERSION = "b2o-compiler-33"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -1069,8 +1069,13 @@ class _Gen:
     def kernel_fn(self, n: NestPlan) -> list[str]:
         out = self._kernel_fn(n)
         assert out[0].rstrip().endswith("{"), out[0]
-        # first statement of every kernel: programmatic-dependent-launch entry
-        return [out[0], "  b2o_pdl_enter();"] + out[1:]
+        # first statement of every kernel: programmatic-dependent-launch entry.
+        # Memory-bound kernels let their dependents launch at once (the waiting
+        # CTAs cost nothing there); the compute-bound k-tile kernel triggers
+        # them only before its stores (b2o_pdl_trigger in ktile_kernel_fn), so
+        # early dependents do not take issue slots from its FMA loop
+        entry = "  b2o_pdl_wait();" if n.shape == "ktile" else "  b2o_pdl_enter();"
+        return [out[0], entry] + out[1:]
 
     def _kernel_fn(self, n: NestPlan) -> list[str]:
         if n.shape == "stencil":
@@ -1709,6 +1714,7 @@ class _Gen:
         out.append("    }")
         out.append("  }")
         emit(post, False, "  ")
+        out.append("  b2o_pdl_trigger();")
         for v in sorted(kp["accs"]):
             for p_ in range(R):
                 for q_ in range(R):
