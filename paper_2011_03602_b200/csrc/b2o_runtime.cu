@@ -318,6 +318,26 @@ void copy_d2h(AppDev *d, int v, bool async_ok = false) {
     d->host_touched[v] = 1;
     return;
   }
+  if (!VI(d, v).is_array && async_ok && d->async_d2h) {
+    // a planned scalar download (e.g. a loop index after a GPU nest) does not
+    // stall the host walk: every host reader of the cell waits for its event
+    wait_host(d, v, SIZE_MAX);
+    AppDev::Pending &p = d->pend[v];
+    if (p.ev.empty()) {
+      cudaEvent_t e;
+      if (!cuda_ok(d, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "D2H event")) return;
+      p.ev.push_back(e);
+    }
+    cuda_ok(d, cudaMemcpyAsync(d->host[v], (char *)d->slab + 8 * v, bytes, cudaMemcpyDeviceToHost, d->w->stream),
+            "D2H scalar copy");
+    cuda_ok(d, cudaEventRecord(p.ev[0], d->w->stream), "D2H scalar event");
+    p.n = 1;
+    p.done = 0;
+    p.chunk = bytes;
+    d->acc.d2h_bytes += bytes;
+    d->host_touched[v] = 1;
+    return;
+  }
   if (VI(d, v).is_array) {
     cuda_ok(d, cudaMemcpyAsync(d->host[v], d->dev[v], var_bytes(d, v), cudaMemcpyDeviceToHost, d->w->stream),
             "D2H copy");
@@ -455,8 +475,12 @@ void cb_pre_launch(b2o_exec *ex, int32_t loop) {
   const b2o_loop_info &li = d->app->info->loops[loop];
   for (int i = 0; i < li.reads.n && !ex->stop; ++i) {
     int v = li.reads.vars[i];
-    if (VI(d, v).is_array) ensure_dev(d, v, &d->acc.unplanned_bytes);
-    else ensure_host(d, v);
+    if (VI(d, v).is_array) {
+      ensure_dev(d, v, &d->acc.unplanned_bytes);
+    } else {
+      wait_host(d, v, SIZE_MAX);  // the launch stub reads the host cell next
+      ensure_host(d, v);
+    }
   }
   for (int i = 0; i < li.writes.n && !ex->stop; ++i) {
     int v = li.writes.vars[i];
