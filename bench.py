@@ -320,6 +320,7 @@ def b200_arm(args, dist: Dist) -> None:
                                "kind": "port", "sample": "the same app run, single-threaded (sequential C semantics)",
                                "cpu_model": cpu_model()} if cpu1_s else None,
         "app_speedup_vs_cpu": round(cpu_s / e2e_s, 2) if cpu_s else None,
+        "app_speedup_vs_cpu_1core": round(cpu1_s / e2e_s, 2) if cpu1_s else None,
         "ga": ga,
         "ops": ops,
         "reductions_opt_in": red,
