@@ -152,6 +152,10 @@ int b2o_histogram(const int32_t *d, int64_t n, void *h, int64_t bins, int elem, 
 int b2o_exact_sum_f32(const float *x, int64_t n, float s0, float *s_out, void *stream);
 size_t b2o_exact_sum_workspace(int64_t n);
 int b2o_exact_sum_f32_ws(const float *x, int64_t n, float s0, float *s_out, void *workspace, void *stream);
+/* the same in fp64: s = (((s0 + x[0]) + x[1]) + ...) in double, bit-identical
+ * to the C loop; the workspace size above covers both formats */
+int b2o_exact_sum_f64(const double *x, int64_t n, double s0, double *s_out, void *stream);
+int b2o_exact_sum_f64_ws(const double *x, int64_t n, double s0, double *s_out, void *workspace, void *stream);
 
 #ifdef __cplusplus
 }

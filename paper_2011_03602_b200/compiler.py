@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-33"
+COMPILER_VERSION = "b2o-compiler-34"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -643,9 +643,10 @@ class _Gen:
 
     def exact_reductions(self, n: NestPlan) -> dict:
         """Reductions of a chained nest that can be summed EXACTLY in loop
-        order on the GPU (b2o_exact_sum_f32, csrc/b2o_xsum.cu): an fp32 scalar
-        whose every update in the nest is ``s = s + e`` / ``s = e + s`` /
-        ``s = s - e`` with ``e`` of C type float (one fp32 addition each), and
+        order on the GPU (b2o_exact_sum_f32 / _f64, csrc/b2o_xsum.cu): an fp32
+        or fp64 scalar whose every update in the nest is ``s = s + e`` /
+        ``s = e + s`` / ``s = s - e`` with ``e`` of the scalar's own C type
+        (one correctly rounded addition each), and
         which every point of the chain updates a compile-time constant
         number of times C (the loops run in-thread below the chain have
         literal bounds).  Point t's j-th update stores its term at
@@ -662,7 +663,9 @@ class _Gen:
             for st in prog.regions[rid].statements:
                 if st.kind == "assign" and st.target[0] == "var" and st.target[1] == v:
                     red = reductions.reduction_stmt(st)
-                    if red is None or etype(prog, red[2], self.precision) != "float":
+                    # one addition in the scalar's own format (an fp32 sum with
+                    # a double term would round twice)
+                    if red is None or etype(prog, red[2], self.precision) != self.T(v):
                         return None
                     total += 1
                 elif st.kind == "loop":
@@ -685,7 +688,7 @@ class _Gen:
 
         out = {}
         for v in sorted(n.reds):
-            if self.T(v) != "float":
+            if self.T(v) not in ("float", "double"):
                 continue
             c = count(prog.loops[n.chain[-1]].body, v)
             if not c:
@@ -960,7 +963,7 @@ class _Gen:
         for v in n.scalar_args:
             out.append(f"  {self.T(v)} s{v};")
         for v in (n.exact or {}):
-            out.append(f"  float *xb{v};  // per-point terms of reduction {self.prog.vars[v].name}, loop order")
+            out.append(f"  {self.T(v)} *xb{v};  // per-point terms of reduction {self.prog.vars[v].name}, loop order")
         out.append(f"}} KA_L{n.root};")
         return out
 
@@ -1036,10 +1039,10 @@ class _Gen:
             out.append(f"  {{ uint64_t g = (total + {per - 1}) / {per}; geom[0] = (uint32_t)(g > {cap}u ? "
                        f"{cap}u : g); geom[1] = geom[2] = 1; geom[3] = {bt}; geom[4] = geom[5] = 1; }}")
         for v, (slot, cnt) in (n.exact or {}).items():
-            out.append(f"  a.xb{v} = (float *)ex->red_buf(ex, {slot}, (int64_t)total * {cnt}); if (ex->stop) return;")
+            out.append(f"  a.xb{v} = ({self.T(v)} *)ex->red_buf(ex, {slot}, (int64_t)total * {cnt}); if (ex->stop) return;")
         out.append(f"  ex->launch(ex, {lid}, &a, (uint32_t)sizeof a, geom);")
         for v, (slot, cnt) in (n.exact or {}).items():
-            out.append(f"  if (!ex->stop) ex->red_exact(ex, {v}, {slot}, (int64_t)total * {cnt}, a.s{v});")
+            out.append(f"  if (!ex->stop) ex->red_exact(ex, {v}, {slot}, (int64_t)total * {cnt}, (double)a.s{v});")
         out.append("}")
         return out
 
@@ -1959,10 +1962,11 @@ class _Gen:
                     v, op, e = red
                     sign = "-" if op == "-" else ""
                     cnt = self._exact[v][1]
+                    T = self.T(v)
                     if cnt == 1:
-                        out.append(pad + f"a.xb{v}[t] = {sign}(float)({self.dev_expr(e)});")
+                        out.append(pad + f"a.xb{v}[t] = {sign}({T})({self.dev_expr(e)});")
                     else:
-                        out.append(pad + f"a.xb{v}[(size_t)t * {cnt}u + xc{v}++] = {sign}(float)({self.dev_expr(e)});")
+                        out.append(pad + f"a.xb{v}[(size_t)t * {cnt}u + xc{v}++] = {sign}({T})({self.dev_expr(e)});")
                 elif red is not None and red[0] in self._reds:
                     v, op, e = red
                     out.append(pad + f"rd{v} = rd{v} {op} ({self.dev_expr(e)});")

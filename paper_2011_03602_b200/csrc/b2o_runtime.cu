@@ -438,7 +438,7 @@ bool red_reserve(AppDev *d, int32_t slot, int64_t n) {
     if (d->red_bufs[slot]) cudaFree(d->red_bufs[slot]);
     d->red_bufs[slot] = nullptr;
     d->red_buf_elems[slot] = 0;
-    if (!cuda_ok(d, cudaMalloc(&d->red_bufs[slot], sizeof(float) * (size_t)std::max<int64_t>(n, 1)),
+    if (!cuda_ok(d, cudaMalloc(&d->red_bufs[slot], sizeof(double) * (size_t)std::max<int64_t>(n, 1)),
                  "exact reduction buffer"))
       return false;
     d->red_buf_elems[slot] = n;
@@ -459,14 +459,19 @@ void *cb_red_buf(b2o_exec *ex, int32_t slot, int64_t n) {
   return red_reserve(d, slot, n) ? d->red_bufs[slot] : nullptr;
 }
 
-void cb_red_exact(b2o_exec *ex, int32_t var, int32_t slot, int64_t n, float s0) {
+void cb_red_exact(b2o_exec *ex, int32_t var, int32_t slot, int64_t n, double s0) {
   AppDev *d = D(ex);
   if (slot >= (int32_t)d->red_bufs.size() || !d->red_bufs[slot]) {
     set_error(d, B2O_RUNTIME_ERROR, "exact reduction without its term buffer");
     return;
   }
-  if (b2o_exact_sum_f32_ws((const float *)d->red_bufs[slot], n, s0, (float *)((char *)d->slab + 8 * var),
-                           d->xsum_ws, d->w->stream) != 0)
+  void *cell = (char *)d->slab + 8 * var;
+  const int rc = VI(d, var).elem == B2O_F64
+                     ? b2o_exact_sum_f64_ws((const double *)d->red_bufs[slot], n, s0, (double *)cell, d->xsum_ws,
+                                            d->w->stream)
+                     : b2o_exact_sum_f32_ws((const float *)d->red_bufs[slot], n, (float)s0, (float *)cell,
+                                            d->xsum_ws, d->w->stream);
+  if (rc != 0)
     cuda_ok(d, cudaGetLastError() == cudaSuccess ? cudaErrorUnknown : cudaGetLastError(), "exact in-order sum");
 }
 

@@ -45,6 +45,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstdint>
 #include <mutex>
 #include <map>
@@ -58,49 +59,85 @@ constexpr int XS_PER_LANE = XS_CHUNK / 32;
 constexpr int XS_SUPER = 32;         // chunks per super-chunk (one CTA of 32 warps)
 constexpr int XS_W = 4;              // binades in each super-chunk's window
 
+// The two IEEE formats: value type, raw bits, the signed integer that holds a
+// run's increments, the fraction width and exponent field.
+struct F32 {
+  using V = float;
+  using U = uint32_t;
+  using I = int;
+  static constexpr int MANT = 23, EMASK = 0xFF, BIAS = 127;
+  static constexpr I kLoEmpty = 0x7FFFFFFF, kHiEmpty = -0x7FFFFFFF - 1, kBig = 1 << 25;
+  static __device__ __forceinline__ U bits(V v) { return __float_as_uint(v); }
+  static __device__ __forceinline__ V value(U b) { return __uint_as_float(b); }
+  static __device__ __forceinline__ V add(V a, V b) { return __fadd_rn(a, b); }
+};
+struct F64 {
+  using V = double;
+  using U = unsigned long long;
+  using I = long long;
+  static constexpr int MANT = 52, EMASK = 0x7FF, BIAS = 1023;
+  static constexpr I kLoEmpty = 0x7FFFFFFFFFFFFFFFLL, kHiEmpty = -0x7FFFFFFFFFFFFFFFLL - 1, kBig = 1LL << 54;
+  static __device__ __forceinline__ U bits(V v) { return (U)__double_as_longlong(v); }
+  static __device__ __forceinline__ V value(U b) { return __longlong_as_double((long long)b); }
+  static __device__ __forceinline__ V add(V a, V b) { return __dadd_rn(a, b); }
+};
+
 // A run's effect for one binade, in units u, for both parities of the
 // running integer S at the run's start (variant p: S odd iff p = 1): a term
 // exactly half-way between two multiples of u rounds to the even neighbour,
 // so its increment depends on the parity of S there -- and after it S is
 // even, whichever way it went.  Tracking both start parities keeps ties on
 // the fast path; merging runs maps each start parity through the first run's
-// end parity.  Valid summaries have |P|, |lo|, |hi| <= 2^24 + 1 (the running
-// integer stays in [2^23, 2^24)); larger ones are flagged, which also keeps
-// every int32 sum below overflow.
-struct Summ {
-  int P0, P1;    // sum of the increments
-  int lo0, lo1;  // min over j of (P_(j+1) - 1)
-  int hi0, hi1;  // max over j of (P_(j+1) + 1)
-  int flags;     // nonzero: unusable for this binade
+// end parity.  Valid summaries have |P|, |lo|, |hi| <= 2^(MANT+1) + 1 (the
+// running integer stays in [2^MANT, 2^(MANT+1))); larger ones are flagged,
+// which also keeps every integer sum below overflow.
+template <class T>
+struct alignas(16) Summ {
+  typename T::I P0, P1;    // sum of the increments
+  typename T::I lo0, lo1;  // min over j of (P_(j+1) - 1)
+  typename T::I hi0, hi1;  // max over j of (P_(j+1) + 1)
+  int flags;               // nonzero: unusable for this binade
   int pad;
 };
 
-constexpr int kLoEmpty = 0x7FFFFFFF, kHiEmpty = -0x7FFFFFFF - 1;
-constexpr int kBig = 1 << 25;
+template <class T>
+__device__ __forceinline__ Summ<T> empty_summ() {
+  return Summ<T>{0, 0, T::kLoEmpty, T::kLoEmpty, T::kHiEmpty, T::kHiEmpty, 0, 0};
+}
+template <class T>
+__device__ __forceinline__ Summ<T> invalid_summ() {
+  return Summ<T>{0, 0, 0, 0, 0, 0, 1, 0};
+}
 
-// x / 2^(e-23) rounded to nearest, as raw bits: returns round(X) (tie = 0) or
-// floor(X) for a half-way X (tie = 1; the increment is floor(X) + the parity
-// of S + floor(X)).  Branch-free (the lanes of a warp evaluate different
-// binades).  |x| >= 2^(e+1) (d > 0) can never keep the sum in the binade and
-// inf / nan are flagged.
-__device__ __forceinline__ int units(uint32_t bits, int e, int &tie, int &flag) {
-  const uint32_t exr = (bits >> 23) & 0xFFu;
-  const uint32_t m = (bits & 0x7FFFFFu) | (exr ? 0x800000u : 0u);
-  const int ex = exr ? (int)exr - 127 : -126;
+// x / 2^(e-MANT) rounded to nearest, as raw bits: returns round(X) (tie = 0)
+// or floor(X) for a half-way X (tie = 1; the increment is floor(X) + the
+// parity of S + floor(X)).  Branch-free (the lanes of a warp evaluate
+// different binades).  |x| >= 2^(e+1) (d > 0) can never keep the sum in the
+// binade and inf / nan are flagged.
+template <class T>
+__device__ __forceinline__ typename T::I units(typename T::U bits, int e, int &tie, int &flag) {
+  using U = typename T::U;
+  using I = typename T::I;
+  constexpr int W = 8 * (int)sizeof(U);
+  const int exr = (int)((bits >> T::MANT) & (U)T::EMASK);
+  const U m = (bits & (((U)1 << T::MANT) - 1)) | (exr ? ((U)1 << T::MANT) : (U)0);
+  const int ex = exr ? exr - T::BIAS : 1 - T::BIAS;
   const int d = ex - e;
-  const int sh = min(max(-d, 1), 31);
-  const uint32_t q = m >> sh, rem = m & ((1u << sh) - 1u), half = 1u << (sh - 1);
-  flag |= (exr == 0xFFu) | (d > 0);
-  const bool neg = (bits >> 31) != 0;
+  const int sh = min(max(-d, 1), W - 1);
+  const U q = m >> sh, rem = m & (((U)1 << sh) - 1), half = (U)1 << (sh - 1);
+  flag |= (exr == T::EMASK) | (d > 0);
+  const bool neg = (bits >> (W - 1)) != 0;
   tie = (d < 0 && rem == half) ? 1 : 0;
-  if (tie) return neg ? -(int)q - 1 : (int)q;  // floor(X)
-  const int r = d == 0 ? (int)m : (d < 0 ? (int)q + (rem > half ? 1 : 0) : 0);
+  if (tie) return neg ? -(I)q - 1 : (I)q;  // floor(X)
+  const I r = d == 0 ? (I)m : (d < 0 ? (I)q + (rem > half ? 1 : 0) : 0);
   return neg ? -r : r;
 }
 
 // apply one term (c, tie) to both variants
-__device__ __forceinline__ void step(Summ &s, int c, int tie) {
-  const int r0 = c + (tie & (s.P0 + c)), r1 = c + (tie & (1 + s.P1 + c));
+template <class T>
+__device__ __forceinline__ void step(Summ<T> &s, typename T::I c, int tie) {
+  using I = typename T::I;
+  const I r0 = c + ((I)tie & (s.P0 + c)), r1 = c + ((I)tie & (1 + s.P1 + c));
   s.P0 += r0;
   s.P1 += r1;
   s.lo0 = min(s.lo0, s.P0 - 1);
@@ -109,53 +146,55 @@ __device__ __forceinline__ void step(Summ &s, int c, int tie) {
   s.hi1 = max(s.hi1, s.P1 + 1);
 }
 
-__device__ __forceinline__ bool out_of_range(int v) { return v > kBig || v < -kBig; }
-
-__device__ __forceinline__ bool big(const Summ &a) {
-  return out_of_range(a.P0) || out_of_range(a.P1) || out_of_range(a.lo0) || out_of_range(a.lo1) ||
-         out_of_range(a.hi0) || out_of_range(a.hi1);
+template <class T>
+__device__ __forceinline__ bool big(const Summ<T> &a) {
+  auto out = [](typename T::I v) { return v > T::kBig || v < -T::kBig; };
+  return out(a.P0) || out(a.P1) || out(a.lo0) || out(a.lo1) || out(a.hi0) || out(a.hi1);
 }
-
-#define kEmpty (Summ{0, 0, kLoEmpty, kLoEmpty, kHiEmpty, kHiEmpty, 0, 0})
-#define kInvalid (Summ{0, 0, 0, 0, 0, 0, 1, 0})
 
 // a then b: variant p of a ends with parity (p + a.P_p) & 1, which selects b's
-__device__ __forceinline__ Summ merge(const Summ &a, const Summ &b) {
-  if (b.lo0 == kLoEmpty) return a;
-  if (a.lo0 == kLoEmpty) return b;
-  if (a.flags | b.flags || big(a) || big(b)) return kInvalid;
+template <class T>
+__device__ __forceinline__ Summ<T> merge(const Summ<T> &a, const Summ<T> &b) {
+  using I = typename T::I;
+  if (b.lo0 == T::kLoEmpty) return a;
+  if (a.lo0 == T::kLoEmpty) return b;
+  if (a.flags | b.flags || big<T>(a) || big<T>(b)) return invalid_summ<T>();
   const bool x0 = (a.P0 & 1) != 0, x1 = ((1 + a.P1) & 1) != 0;
-  const int bP0 = x0 ? b.P1 : b.P0, bl0 = x0 ? b.lo1 : b.lo0, bh0 = x0 ? b.hi1 : b.hi0;
-  const int bP1 = x1 ? b.P1 : b.P0, bl1 = x1 ? b.lo1 : b.lo0, bh1 = x1 ? b.hi1 : b.hi0;
-  return Summ{a.P0 + bP0, a.P1 + bP1, min(a.lo0, a.P0 + bl0), min(a.lo1, a.P1 + bl1),
-              max(a.hi0, a.P0 + bh0), max(a.hi1, a.P1 + bh1), 0, 0};
+  const I bP0 = x0 ? b.P1 : b.P0, bl0 = x0 ? b.lo1 : b.lo0, bh0 = x0 ? b.hi1 : b.hi0;
+  const I bP1 = x1 ? b.P1 : b.P0, bl1 = x1 ? b.lo1 : b.lo0, bh1 = x1 ? b.hi1 : b.hi0;
+  return Summ<T>{a.P0 + bP0, a.P1 + bP1, min(a.lo0, a.P0 + bl0), min(a.lo1, a.P1 + bl1),
+                 max(a.hi0, a.P0 + bh0), max(a.hi1, a.P1 + bh1), 0, 0};
 }
 
-__device__ __forceinline__ Summ shfl_down_summ(const Summ &s, int d) {
-  return Summ{__shfl_down_sync(0xffffffffu, s.P0, d), __shfl_down_sync(0xffffffffu, s.P1, d),
-              __shfl_down_sync(0xffffffffu, s.lo0, d), __shfl_down_sync(0xffffffffu, s.lo1, d),
-              __shfl_down_sync(0xffffffffu, s.hi0, d), __shfl_down_sync(0xffffffffu, s.hi1, d),
-              __shfl_down_sync(0xffffffffu, s.flags, d), 0};
+template <class T>
+__device__ __forceinline__ Summ<T> shfl_down_summ(const Summ<T> &s, int d) {
+  return Summ<T>{__shfl_down_sync(0xffffffffu, s.P0, d), __shfl_down_sync(0xffffffffu, s.P1, d),
+                 __shfl_down_sync(0xffffffffu, s.lo0, d), __shfl_down_sync(0xffffffffu, s.lo1, d),
+                 __shfl_down_sync(0xffffffffu, s.hi0, d), __shfl_down_sync(0xffffffffu, s.hi1, d),
+                 __shfl_down_sync(0xffffffffu, s.flags, d), 0};
 }
 
-__device__ __forceinline__ Summ shfl_up_summ(const Summ &s, int d) {
-  return Summ{__shfl_up_sync(0xffffffffu, s.P0, d), __shfl_up_sync(0xffffffffu, s.P1, d),
-              __shfl_up_sync(0xffffffffu, s.lo0, d), __shfl_up_sync(0xffffffffu, s.lo1, d),
-              __shfl_up_sync(0xffffffffu, s.hi0, d), __shfl_up_sync(0xffffffffu, s.hi1, d),
-              __shfl_up_sync(0xffffffffu, s.flags, d), 0};
+template <class T>
+__device__ __forceinline__ Summ<T> shfl_up_summ(const Summ<T> &s, int d) {
+  return Summ<T>{__shfl_up_sync(0xffffffffu, s.P0, d), __shfl_up_sync(0xffffffffu, s.P1, d),
+                 __shfl_up_sync(0xffffffffu, s.lo0, d), __shfl_up_sync(0xffffffffu, s.lo1, d),
+                 __shfl_up_sync(0xffffffffu, s.hi0, d), __shfl_up_sync(0xffffffffu, s.hi1, d),
+                 __shfl_up_sync(0xffffffffu, s.flags, d), 0};
 }
 
-__device__ __forceinline__ Summ shfl_summ(const Summ &s, int src) {
-  return Summ{__shfl_sync(0xffffffffu, s.P0, src), __shfl_sync(0xffffffffu, s.P1, src),
-              __shfl_sync(0xffffffffu, s.lo0, src), __shfl_sync(0xffffffffu, s.lo1, src),
-              __shfl_sync(0xffffffffu, s.hi0, src), __shfl_sync(0xffffffffu, s.hi1, src),
-              __shfl_sync(0xffffffffu, s.flags, src), 0};
+template <class T>
+__device__ __forceinline__ Summ<T> shfl_summ(const Summ<T> &s, int src) {
+  return Summ<T>{__shfl_sync(0xffffffffu, s.P0, src), __shfl_sync(0xffffffffu, s.P1, src),
+                 __shfl_sync(0xffffffffu, s.lo0, src), __shfl_sync(0xffffffffu, s.lo1, src),
+                 __shfl_sync(0xffffffffu, s.hi0, src), __shfl_sync(0xffffffffu, s.hi1, src),
+                 __shfl_sync(0xffffffffu, s.flags, src), 0};
 }
 
 // A: per super-chunk (double): its sum, and how far the running sum can get
 // from the super-chunk's starting value: the extreme prefix sums at chunk
 // boundaries plus the largest chunk magnitude (a chunk's own excursion)
-__global__ void __launch_bounds__(256) xs_stats_kernel(const float *__restrict__ x, int64_t n,
+template <class T>
+__global__ void __launch_bounds__(256) xs_stats_kernel(const typename T::V *__restrict__ x, int64_t n,
                                                         double *__restrict__ ssum, double *__restrict__ sreach) {
   __shared__ double cs[XS_SUPER], ca[XS_SUPER];
   const int64_t b0 = (int64_t)blockIdx.x * XS_SUPER * XS_CHUNK;
@@ -200,12 +239,12 @@ __global__ void __launch_bounds__(256) xs_stats_kernel(const float *__restrict__
 // A2: each super-chunk's binade window.  est = s0 + sum of the earlier
 // super-chunks (double); |s| inside the super-chunk is at most
 // max(|est + lo|, |est + hi|) + the largest chunk magnitude, with 25 % slack
-// for the drift of the fp32 running sum from the exact one; the window is the
+// for the drift of the running sum from the exact one; the window is the
 // XS_W binades up to that bound (a running sum below it is added element by
 // element: exact, only slower).
 __global__ void __launch_bounds__(1024) xs_window_kernel(const double *__restrict__ ssum,
                                                           const double *__restrict__ sreach, int64_t nsupers,
-                                                          float s0, int *__restrict__ ebase) {
+                                                          double s0, int *__restrict__ ebase) {
   __shared__ double part[1024];
   const int t = threadIdx.x;
   const int64_t per = (nsupers + 1023) / 1024;
@@ -220,10 +259,10 @@ __global__ void __launch_bounds__(1024) xs_window_kernel(const double *__restric
     part[t] += v;
     __syncthreads();
   }
-  double est = (double)s0 + (t > 0 ? part[t - 1] : 0.0);
+  double est = s0 + (t > 0 ? part[t - 1] : 0.0);
   for (int64_t i = i0; i < i1; ++i) {
     const double reach = fmax(fabs(est + sreach[3 * i]), fabs(est + sreach[3 * i + 1])) + sreach[3 * i + 2];
-    const double top = reach * 1.25 + 1e-30;
+    const double top = reach * 1.25 + 1e-300;
     int e;
     frexp(top, &e);  // top in [2^(e-1), 2^e)
     ebase[i] = (e - 1) - (XS_W - 1);
@@ -234,55 +273,60 @@ __global__ void __launch_bounds__(1024) xs_window_kernel(const double *__restric
 // B: chunk and super-chunk summaries for the XS_W window binades of their
 // super-chunk.  A warp owns a chunk: lane = 4 * part + k runs binade
 // ebase + k over part (32 elements) of the chunk; the 8 parts are merged in
-// order with three shuffles.
-__global__ void __launch_bounds__(1024) xs_summ_kernel(const float *__restrict__ x, int64_t n,
-                                                        const int *__restrict__ ebase, Summ *__restrict__ chunks,
-                                                        Summ *__restrict__ supers, int64_t nchunks) {
-  __shared__ float xs[XS_SUPER][XS_CHUNK + XS_CHUNK / 32];
-  __shared__ Summ sm[XS_SUPER][XS_W];
+// order with three shuffles.  The chunk is staged in (dynamic) shared memory.
+template <class T>
+__global__ void __launch_bounds__(1024) xs_summ_kernel(const typename T::V *__restrict__ x, int64_t n,
+                                                        const int *__restrict__ ebase, Summ<T> *__restrict__ chunks,
+                                                        Summ<T> *__restrict__ supers, int64_t nchunks) {
+  using V = typename T::V;
+  using I = typename T::I;
+  constexpr int ROW = XS_CHUNK + XS_CHUNK / 32;
+  extern __shared__ __align__(16) unsigned char xs_raw[];
+  V *xs = reinterpret_cast<V *>(xs_raw);
+  __shared__ Summ<T> sm[XS_SUPER][XS_W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * XS_SUPER + warp;
   const int64_t base = c * XS_CHUNK;
   const int cnt = c < nchunks ? (int)min((int64_t)XS_CHUNK, n - base) : 0;
+  V *my = xs + warp * ROW;
 #pragma unroll
   for (int j = 0; j < XS_PER_LANE; ++j) {
     const int i = lane + 32 * j;
-    xs[warp][i + (i >> 5)] = i < cnt ? x[base + i] : 0.f;  // parts in different banks
+    my[i + (i >> 5)] = i < cnt ? x[base + i] : (V)0;  // parts in different banks
   }
   __syncwarp();
   const int k = lane & (XS_W - 1), part = lane >> 2;
   const int e = ebase[blockIdx.x] + k;
   constexpr int PART = XS_CHUNK / 8;
-  Summ s = kEmpty;
+  Summ<T> s = empty_summ<T>();
   int flag = 0;
   const int i0 = part * PART, i1 = min(i0 + PART, cnt);
-  const float *row = &xs[warp][part * (PART + 1)];
-  if (i1 > i0) s = Summ{0, 0, kLoEmpty, kLoEmpty, kHiEmpty, kHiEmpty, 0, 0};
+  const V *row = my + part * (PART + 1);
   if (i1 - i0 == PART) {
 #pragma unroll 4
     for (int i = 0; i < PART; i += 8) {
-      uint32_t b[8];
+      typename T::U b[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = __float_as_uint(row[i + j]);
+      for (int j = 0; j < 8; ++j) b[j] = T::bits(row[i + j]);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         int tie;
-        const int c = units(b[j], e, tie, flag);  // |P| < 32 * 2^24: no overflow
-        step(s, c, tie);
+        const I cc = units<T>(b[j], e, tie, flag);  // |P| < 32 * 2^(MANT+1): no overflow
+        step<T>(s, cc, tie);
       }
     }
   } else {
     for (int i = 0; i < i1 - i0; ++i) {
       int tie;
-      const int c = units(__float_as_uint(row[i]), e, tie, flag);
-      step(s, c, tie);
+      const I cc = units<T>(T::bits(row[i]), e, tie, flag);
+      step<T>(s, cc, tie);
     }
   }
   s.flags = flag;
 #pragma unroll
   for (int d = 4; d < 32; d <<= 1) {  // ordered merge: part p with part p + d/4
-    const Summ t = shfl_down_summ(s, d);
-    if ((part & (2 * (d >> 2) - 1)) == 0) s = merge(s, t);
+    const Summ<T> t = shfl_down_summ<T>(s, d);
+    if ((part & (2 * (d >> 2) - 1)) == 0) s = merge<T>(s, t);
   }
   if (lane < XS_W) {
     if (c < nchunks) chunks[c * XS_W + k] = s;
@@ -291,26 +335,30 @@ __global__ void __launch_bounds__(1024) xs_summ_kernel(const float *__restrict__
   __syncthreads();
   if (threadIdx.x < XS_W) {
     const int kk = threadIdx.x;
-    Summ a = sm[0][kk];
-    for (int w = 1; w < XS_SUPER; ++w) a = merge(a, sm[w][kk]);
+    Summ<T> a = sm[0][kk];
+    for (int w = 1; w < XS_SUPER; ++w) a = merge<T>(a, sm[w][kk]);
     supers[(int64_t)blockIdx.x * XS_W + kk] = a;
   }
 }
 
 // ---- C: the in-order walk (one warp) -------------------------------------
 
+template <class T>
 struct WalkState {
-  bool ok;   // s is a normal float
-  int e;     // its binade: |s| in [2^e, 2^(e+1))
-  int S;     // |s| / 2^(e-23), in [2^23, 2^24)
+  bool ok;            // s is a normal number
+  int e;              // its binade: |s| in [2^e, 2^(e+1))
+  typename T::I S;    // |s| / 2^(e-MANT), in [2^MANT, 2^(MANT+1))
   bool neg;
 };
 
-__device__ __forceinline__ WalkState state_of(float s) {
-  const uint32_t bits = __float_as_uint(s);
-  const uint32_t exr = (bits >> 23) & 0xFFu;
-  return WalkState{exr != 0 && exr != 0xFFu, (int)exr - 127, (int)((bits & 0x7FFFFFu) | 0x800000u),
-                   (bits >> 31) != 0};
+template <class T>
+__device__ __forceinline__ WalkState<T> state_of(typename T::V s) {
+  using U = typename T::U;
+  const U b = T::bits(s);
+  const int exr = (int)((b >> T::MANT) & (U)T::EMASK);
+  return WalkState<T>{exr != 0 && exr != T::EMASK, exr - T::BIAS,
+                      (typename T::I)((b & (((U)1 << T::MANT) - 1)) | ((U)1 << T::MANT)),
+                      (b >> (8 * sizeof(U) - 1)) != 0};
 }
 
 // a run summary (for s's binade) is usable from state w: the variant of S's
@@ -318,36 +366,44 @@ __device__ __forceinline__ WalkState state_of(float s) {
 // increments negate (ties included, round-half-even being symmetric) and the
 // parity evolution is the same, so the prefix range flips (|S| - hi,
 // |S| - lo) and S' = |S| - P.
-__device__ __forceinline__ bool usable(const Summ &t, const WalkState &w) {
+template <class T>
+__device__ __forceinline__ bool usable(const Summ<T> &t, const WalkState<T> &w) {
+  using I = typename T::I;
+  constexpr I lo_lim = (I)1 << T::MANT, hi_lim = (I)1 << (T::MANT + 1);
   if (t.flags) return false;
-  if (t.lo0 == kLoEmpty) return true;
+  if (t.lo0 == T::kLoEmpty) return true;
   const bool odd = (w.S & 1) != 0;
-  const int lo = odd ? t.lo1 : t.lo0, hi = odd ? t.hi1 : t.hi0;
-  return w.neg ? (w.S - hi >= (1 << 23) && w.S - lo <= (1 << 24))
-               : (w.S + lo >= (1 << 23) && w.S + hi <= (1 << 24));
+  const I lo = odd ? t.lo1 : t.lo0, hi = odd ? t.hi1 : t.hi0;
+  return w.neg ? (w.S - hi >= lo_lim && w.S - lo <= hi_lim) : (w.S + lo >= lo_lim && w.S + hi <= hi_lim);
 }
 
-__device__ __forceinline__ float advance(float s, const Summ &t, const WalkState &w) {
-  if (t.lo0 == kLoEmpty) return s;
-  const int P = (w.S & 1) ? t.P1 : t.P0;
-  const int S2 = w.neg ? w.S - P : w.S + P;
-  return __uint_as_float((__float_as_uint(s) & 0xFF800000u) | (uint32_t)(S2 - (1 << 23)));
+template <class T>
+__device__ __forceinline__ typename T::V advance(typename T::V s, const Summ<T> &t, const WalkState<T> &w) {
+  using U = typename T::U;
+  using I = typename T::I;
+  if (t.lo0 == T::kLoEmpty) return s;
+  const I P = (w.S & 1) ? t.P1 : t.P0;
+  const I S2 = w.neg ? w.S - P : w.S + P;
+  const U keep = ~(((U)1 << T::MANT) - 1);  // sign and exponent
+  return T::value((T::bits(s) & keep) | (U)(S2 - ((I)1 << T::MANT)));
 }
 
-// lane i holds the summary (for s's binade) of run i: kEmpty outside
-// [first, cnt), kInvalid when its window lacks the binade.  Applies the
+// lane i holds the summary (for s's binade) of run i: empty outside
+// [first, cnt), invalid when its window lacks the binade.  Applies the
 // longest usable prefix of runs first.. to s; returns how many runs that was.
-__device__ __forceinline__ int scan_apply(float &s, Summ mine, int first, int cnt, const WalkState &w) {
+template <class T>
+__device__ __forceinline__ int scan_apply(typename T::V &s, Summ<T> mine, int first, int cnt,
+                                          const WalkState<T> &w) {
   const int lane = threadIdx.x & 31;
-  Summ pre = mine;
+  Summ<T> pre = mine;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const Summ t = shfl_up_summ(pre, d);
-    if (lane >= d) pre = merge(t, pre);
+    const Summ<T> t = shfl_up_summ<T>(pre, d);
+    if (lane >= d) pre = merge<T>(t, pre);
   }
-  const unsigned bad = __ballot_sync(0xffffffffu, lane >= first && lane < cnt && !usable(pre, w));
+  const unsigned bad = __ballot_sync(0xffffffffu, lane >= first && lane < cnt && !usable<T>(pre, w));
   const int f = bad ? __ffs(bad) - 1 : cnt;
-  if (f > first) s = advance(s, shfl_summ(pre, f - 1), w);
+  if (f > first) s = advance<T>(s, shfl_summ<T>(pre, f - 1), w);
   return f - first;
 }
 
@@ -355,18 +411,20 @@ __device__ __forceinline__ int scan_apply(float &s, Summ mine, int first, int cn
 // i's record for s's binade, a warp scan merges them in order and the
 // longest usable prefix is applied in O(1).  A super-chunk that is not
 // usable is walked by its 32 chunks the same way; a chunk that is not usable
-// either (binade crossing, tie, s outside its window or not normal) is added
-// element by element with __fadd_rn -- the definition.  The next group's
-// records are loaded while the current group is walked.
-__global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict__ x, int64_t n,
-                                                         const int *__restrict__ ebase, float s0,
-                                                         const Summ *__restrict__ chunks,
-                                                         const Summ *__restrict__ supers, int64_t nchunks,
-                                                         int64_t nsupers, float *out, int stats) {
-  constexpr int R4 = (int)(sizeof(Summ) / sizeof(int4));  // int4 per record
+// either (binade crossing, s outside its window or not normal) is added
+// element by element with a correctly rounded add -- the definition.  The
+// next group's records are loaded while the current group is walked.
+template <class T>
+__global__ void __launch_bounds__(32) xs_compose_kernel(const typename T::V *__restrict__ x, int64_t n,
+                                                         const int *__restrict__ ebase, typename T::V s0,
+                                                         const Summ<T> *__restrict__ chunks,
+                                                         const Summ<T> *__restrict__ supers, int64_t nchunks,
+                                                         int64_t nsupers, typename T::V *out, int stats) {
+  using V = typename T::V;
+  constexpr int R4 = (int)(sizeof(Summ<T>) / sizeof(int4));  // int4 per record
   __shared__ int4 sbuf[2][32 * XS_W * R4];
   __shared__ int4 cbuf[XS_SUPER * XS_W * R4];
-  __shared__ __align__(16) float xbuf[XS_CHUNK];
+  __shared__ __align__(16) V xbuf[XS_CHUNK];
   const int lane = threadIdx.x;
   const int4 *sup4 = reinterpret_cast<const int4 *>(supers);
   const int4 *chk4 = reinterpret_cast<const int4 *>(chunks);
@@ -385,7 +443,7 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
 #pragma unroll
     for (int j = 0; j < XS_W * R4; ++j) sbuf[b][lane + 32 * j] = pre[j];
   };
-  float s = s0;
+  V s = s0;
   const int64_t ngroups = (nsupers + 31) / 32;
   fetch(0);
   stash(0);
@@ -395,14 +453,16 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
     const int cur = (int)(g & 1);
     if (g + 1 < ngroups) fetch(g + 1);
     const int cnt = (int)min((int64_t)32, nsupers - g * 32);
-    const Summ *srec = reinterpret_cast<const Summ *>(sbuf[cur]);
+    const Summ<T> *srec = reinterpret_cast<const Summ<T> *>(sbuf[cur]);
     int pos = 0;
     while (pos < cnt) {
-      WalkState w = state_of(s);
+      WalkState<T> w = state_of<T>(s);
       if (w.ok) {
         const int k = w.e - eb;
-        Summ mine = (lane < pos || lane >= cnt) ? kEmpty : ((k >= 0 && k < XS_W) ? srec[lane * XS_W + k] : kInvalid);
-        pos += scan_apply(s, mine, pos, cnt, w);
+        Summ<T> mine = (lane < pos || lane >= cnt)
+                           ? empty_summ<T>()
+                           : ((k >= 0 && k < XS_W) ? srec[lane * XS_W + k] : invalid_summ<T>());
+        pos += scan_apply<T>(s, mine, pos, cnt, w);
         if (pos >= cnt) break;
       }
       // super-chunk g*32 + pos by its chunks
@@ -418,15 +478,16 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
         cbuf[lane + 32 * j] = r < nchunks * XS_W * R4 ? chk4[r] : make_int4(0, 0, 0, 0);
       }
       __syncwarp();
-      const Summ *crec = reinterpret_cast<const Summ *>(cbuf);
+      const Summ<T> *crec = reinterpret_cast<const Summ<T> *>(cbuf);
       int cpos = 0;
       while (cpos < nc) {
-        w = state_of(s);
+        w = state_of<T>(s);
         if (w.ok) {
           const int k = w.e - ceb;
-          Summ mine = (lane < cpos || lane >= nc) ? kEmpty
-                                                  : ((k >= 0 && k < XS_W) ? crec[lane * XS_W + k] : kInvalid);
-          cpos += scan_apply(s, mine, cpos, nc, w);
+          Summ<T> mine = (lane < cpos || lane >= nc)
+                             ? empty_summ<T>()
+                             : ((k >= 0 && k < XS_W) ? crec[lane * XS_W + k] : invalid_summ<T>());
+          cpos += scan_apply<T>(s, mine, cpos, nc, w);
           if (cpos >= nc) break;
         }
         // chunk c0 + cpos element by element
@@ -436,19 +497,19 @@ __global__ void __launch_bounds__(32) xs_compose_kernel(const float *__restrict_
 #pragma unroll
         for (int j = 0; j < XS_PER_LANE; ++j) {
           const int i = lane + 32 * j;
-          xbuf[i] = i < m ? x[base + i] : 0.f;
+          xbuf[i] = i < m ? x[base + i] : (V)0;
         }
         __syncwarp();
-        const float *xb = xbuf;
         if (lane == 0) {
           int i = 0;
           for (; i + 8 <= m; i += 8) {  // operands fetched ahead of the dependent adds
-            const float4 a = *reinterpret_cast<const float4 *>(&xb[i]);
-            const float4 b = *reinterpret_cast<const float4 *>(&xb[i + 4]);
-            s = __fadd_rn(s, a.x); s = __fadd_rn(s, a.y); s = __fadd_rn(s, a.z); s = __fadd_rn(s, a.w);
-            s = __fadd_rn(s, b.x); s = __fadd_rn(s, b.y); s = __fadd_rn(s, b.z); s = __fadd_rn(s, b.w);
+            V v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = xbuf[i + j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s = T::add(s, v[j]);
           }
-          for (; i < m; ++i) s = __fadd_rn(s, xb[i]);
+          for (; i < m; ++i) s = T::add(s, xbuf[i]);
         }
         s = __shfl_sync(0xffffffffu, s, 0);
         __syncwarp();
@@ -476,13 +537,12 @@ struct Workspace {
 std::mutex ws_mu;
 std::map<int, Workspace> ws_by_dev;
 
-}  // namespace
-
 struct Layout {
   int64_t nchunks, nsupers;
   size_t ssum, sreach, ebase, chunks, supers, bytes;
 };
 
+template <class T>
 Layout layout(int64_t n) {
   Layout L;
   L.nchunks = (n + XS_CHUNK - 1) / XS_CHUNK;
@@ -492,40 +552,49 @@ Layout layout(int64_t n) {
   L.sreach = up(L.ssum + sizeof(double) * L.nsupers);  // (lo, hi, chunk magnitude) per super-chunk
   L.ebase = up(L.sreach + 3 * sizeof(double) * L.nsupers);
   L.chunks = up(L.ebase + sizeof(int) * (L.nsupers + 32));
-  L.supers = up(L.chunks + sizeof(Summ) * XS_W * L.nchunks);
-  L.bytes = up(L.supers + sizeof(Summ) * XS_W * (L.nsupers + 32));
+  L.supers = up(L.chunks + sizeof(Summ<T>) * XS_W * L.nchunks);
+  L.bytes = up(L.supers + sizeof(Summ<T>) * XS_W * (L.nsupers + 32));
   return L;
 }
 
-extern "C" size_t b2o_exact_sum_workspace(int64_t n) { return layout(std::max<int64_t>(n, 1)).bytes; }
-
-// s_out = (((s0 + x[0]) + x[1]) + ...) in fp32, bit-identical to the loop;
-// workspace: device memory of b2o_exact_sum_workspace(n) bytes.
-// Asynchronous on `stream`.
-extern "C" int b2o_exact_sum_f32_ws(const float *x, int64_t n, float s0, float *s_out, void *workspace,
-                                    void *stream) {
+template <class T>
+int exact_sum_ws(const typename T::V *x, int64_t n, typename T::V s0, typename T::V *s_out, void *workspace,
+                 void *stream) {
+  using V = typename T::V;
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 0) return -1;
   if (n == 0) {
-    return cudaMemcpyAsync(s_out, &s0, sizeof(float), cudaMemcpyHostToDevice, st) == cudaSuccess ? 0 : -1;
+    static_assert(sizeof(V) <= 8, "");
+    return cudaMemcpyAsync(s_out, &s0, sizeof(V), cudaMemcpyHostToDevice, st) == cudaSuccess ? 0 : -1;
   }
-  const Layout L = layout(n);
+  const Layout L = layout<T>(n);
   char *ws = (char *)workspace;
   double *ssum = (double *)(ws + L.ssum), *sreach = (double *)(ws + L.sreach);
   int *ebase = (int *)(ws + L.ebase);
-  Summ *chunks = (Summ *)(ws + L.chunks), *supers = (Summ *)(ws + L.supers);
-  xs_stats_kernel<<<(unsigned)L.nsupers, 256, 0, st>>>(x, n, ssum, sreach);
-  xs_window_kernel<<<1, 1024, 0, st>>>(ssum, sreach, L.nsupers, s0, ebase);
-  xs_summ_kernel<<<(unsigned)L.nsupers, 1024, 0, st>>>(x, n, ebase, chunks, supers, L.nchunks);
+  Summ<T> *chunks = (Summ<T> *)(ws + L.chunks), *supers = (Summ<T> *)(ws + L.supers);
+  constexpr int kSummSmem = XS_SUPER * (XS_CHUNK + XS_CHUNK / 32) * (int)sizeof(V);
+  static std::atomic<bool> attr[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    if (cudaFuncSetAttribute(xs_summ_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSummSmem) !=
+        cudaSuccess)
+      return -1;
+    attr[dev & 63] = true;
+  }
+  xs_stats_kernel<T><<<(unsigned)L.nsupers, 256, 0, st>>>(x, n, ssum, sreach);
+  xs_window_kernel<<<1, 1024, 0, st>>>(ssum, sreach, L.nsupers, (double)s0, ebase);
+  xs_summ_kernel<T><<<(unsigned)L.nsupers, 1024, kSummSmem, st>>>(x, n, ebase, chunks, supers, L.nchunks);
   static const int stats = getenv("B2O_XSUM_STATS") != nullptr;
-  xs_compose_kernel<<<1, 32, 0, st>>>(x, n, ebase, s0, chunks, supers, L.nchunks, L.nsupers, s_out, stats);
+  xs_compose_kernel<T><<<1, 32, 0, st>>>(x, n, ebase, s0, chunks, supers, L.nchunks, L.nsupers, s_out, stats);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-extern "C" int b2o_exact_sum_f32(const float *x, int64_t n, float s0, float *s_out, void *stream) {
+template <class T>
+int exact_sum(const typename T::V *x, int64_t n, typename T::V s0, typename T::V *s_out, void *stream) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const size_t need = b2o_exact_sum_workspace(n);
+  const size_t need = layout<T>(std::max<int64_t>(n, 1)).bytes;
   void *ws = nullptr;
   {
     std::lock_guard<std::mutex> lk(ws_mu);
@@ -542,16 +611,45 @@ extern "C" int b2o_exact_sum_f32(const float *x, int64_t n, float s0, float *s_o
     }
     ws = w.p;
   }
-  return b2o_exact_sum_f32_ws(x, n, s0, s_out, ws, stream);
+  return exact_sum_ws<T>(x, n, s0, s_out, ws, stream);
+}
+
+}  // namespace
+
+// workspace bytes for either format (the fp64 records are the larger)
+extern "C" size_t b2o_exact_sum_workspace(int64_t n) { return layout<F64>(std::max<int64_t>(n, 1)).bytes; }
+
+// s_out = (((s0 + x[0]) + x[1]) + ...), each addition rounded to the format,
+// bit-identical to the loop; workspace: device memory of
+// b2o_exact_sum_workspace(n) bytes.  Asynchronous on `stream`.
+extern "C" int b2o_exact_sum_f32_ws(const float *x, int64_t n, float s0, float *s_out, void *workspace,
+                                    void *stream) {
+  return exact_sum_ws<F32>(x, n, s0, s_out, workspace, stream);
+}
+
+extern "C" int b2o_exact_sum_f64_ws(const double *x, int64_t n, double s0, double *s_out, void *workspace,
+                                    void *stream) {
+  return exact_sum_ws<F64>(x, n, s0, s_out, workspace, stream);
+}
+
+extern "C" int b2o_exact_sum_f32(const float *x, int64_t n, float s0, float *s_out, void *stream) {
+  return exact_sum<F32>(x, n, s0, s_out, stream);
+}
+
+extern "C" int b2o_exact_sum_f64(const double *x, int64_t n, double s0, double *s_out, void *stream) {
+  return exact_sum<F64>(x, n, s0, s_out, stream);
 }
 
 // force-load this file's kernels (lazy module loading would otherwise charge
 // the first timed pattern that uses one); called per device by b2o_init
 extern "C" void b2o_xsum_warm(void) {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, xs_stats_kernel);
+  cudaFuncGetAttributes(&a, xs_stats_kernel<F32>);
+  cudaFuncGetAttributes(&a, xs_stats_kernel<F64>);
   cudaFuncGetAttributes(&a, xs_window_kernel);
-  cudaFuncGetAttributes(&a, xs_summ_kernel);
-  cudaFuncGetAttributes(&a, xs_compose_kernel);
+  cudaFuncGetAttributes(&a, xs_summ_kernel<F32>);
+  cudaFuncGetAttributes(&a, xs_summ_kernel<F64>);
+  cudaFuncGetAttributes(&a, xs_compose_kernel<F32>);
+  cudaFuncGetAttributes(&a, xs_compose_kernel<F64>);
   cudaGetLastError();
 }

@@ -112,6 +112,10 @@ def lib() -> ctypes.CDLL:
             "b2o_exact_sum_f32": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_void_p],
                                   ctypes.c_int),
             "b2o_exact_sum_workspace": ([ctypes.c_int64], ctypes.c_size_t),
+            "b2o_exact_sum_f64": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p],
+                                  ctypes.c_int),
+            "b2o_exact_sum_f64_ws": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
             "b2o_exact_sum_f32_ws": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p,
                                      ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
             "b2o_bench_replay": ([ctypes.c_uint64, ctypes.c_int32, ctypes.POINTER(Pattern), ctypes.c_int32,

@@ -72,3 +72,38 @@ def test_exact_sum_differs_from_pairwise():
     want = seq_sum(x, 0.0)
     assert want != np.float32(np.sum(x, dtype=np.float64))
     assert same(gpu_sum(x, 0.0), want)
+
+
+def seq_sum64(x: np.ndarray, s0: float) -> np.float64:
+    return np.add.accumulate(np.concatenate([np.array([s0], np.float64), x.astype(np.float64)]),
+                             dtype=np.float64)[-1]
+
+
+def gpu_sum64(x: np.ndarray, s0: float) -> np.float64:
+    from paper_2011_03602_b200.runtime import lib
+
+    dx = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib().b2o_exact_sum_f64(dx.data_ptr(), dx.numel(), float(s0), out.data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    return out.cpu().numpy()[0]
+
+
+def cases64():
+    r = np.random.default_rng(1106)
+    yield "uniform64", r.random(2_000_003), 0.0
+    yield "squares64", r.standard_normal(1 << 20) ** 2 * 1e-6, 0.0
+    yield "mixed64", r.standard_normal(1 << 19), 3.0
+    yield "ties64", r.integers(0, 64, 1 << 20) * 2.0 ** -10, 1024.0
+    yield "wide64", r.random(1 << 18) * 10.0 ** r.integers(-200, 200, 1 << 18), 0.0
+    yield "subnormal64", np.full(70_000, 1e-310), 0.0
+    yield "ragged64", r.random(256 * 32 * 3 + 17), -5.0
+    yield "small64", r.random(37), 2.0
+
+
+@pytest.mark.parametrize("name,x,s0", list(cases64()), ids=[c[0] for c in cases64()])
+def test_exact_sum_f64_matches_sequential_loop(name, x, s0):
+    want = seq_sum64(x, s0)
+    got = gpu_sum64(x, s0)
+    assert np.float64(got).tobytes() == np.float64(want).tobytes(), (name, got, want)

@@ -51,7 +51,7 @@ def run(precision: str = "fp32") -> None:
     from paper_2011_03602_b200.ir import Program
 
     rec = json.loads(OUT.read_text())
-    bad, tree, n = [], [], 0
+    bad, n = [], 0
     for name, r in rec.items():
         r["spec"]["precision"] = precision
         prog = Program(r["doc"])
@@ -72,17 +72,11 @@ def run(precision: str = "fp32") -> None:
             for vid in outs:
                 got = app.read(vid, worker=res["worker"])
                 if got.tobytes() != np.asarray(want[vid], dtype=got.dtype).tobytes():
-                    # fp64 opt-in reductions use the reassociating tree (the
-                    # exact in-order sum is fp32-only): valid within 1e-12,
-                    # not bit-exact -- counted apart
-                    if precision == "fp64" and r["spec"].get("reductions"):
-                        tree.append((name, g, prog.vars[vid].name))
-                    else:
-                        bad.append((name, g, prog.vars[vid].name))
+                    bad.append((name, g, prog.vars[vid].name))
                     break
         ev.close()
     print(json.dumps({"precision": precision, "programs": len(rec), "genomes": n, "failures": len(bad),
-                      "first": bad[:10], "fp64_tree_reductions_valid_not_bitexact": len(tree)}))
+                      "first": bad[:10]}))
 
 
 if __name__ == "__main__":
