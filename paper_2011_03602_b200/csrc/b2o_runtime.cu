@@ -639,7 +639,10 @@ int load_host_module(AppShared *a) {
   return 0;
 }
 
-int make_replica(AppShared *a, Worker *w, AppDev **out) {
+// src: an existing replica on another worker whose device arrays already
+// hold the initial state -- copied device to device (NVLink peer copy across
+// GPUs, a plain copy on the same GPU) instead of one more PCIe upload
+int make_replica(AppShared *a, Worker *w, AppDev **out, const AppDev *src = nullptr) {
   auto d = std::make_unique<AppDev>();
   d->app = a;
   d->w = w;
@@ -686,14 +689,18 @@ int make_replica(AppShared *a, Worker *w, AppDev **out) {
       return fail("device alloc %zu B for %s", bytes, vi.name);
     cudaMemset(d->dev_alloc[v], 0, bytes + 2 * kB2oGuard);
     d->dev[v] = (char *)d->dev_alloc[v] + kB2oGuard;
-    if (cudaMemcpy(d->dev[v], a->initial[v].data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess)
-      return fail("initial upload of %s", vi.name);
+    memcpy(d->host[v], a->initial[v].data(), bytes);
+    if (src != nullptr) {
+      if (cudaMemcpyPeer(d->dev[v], w->device, src->dev[v], src->w->device, bytes) != cudaSuccess)
+        return fail("initial peer copy of %s", vi.name);
+    } else if (cudaMemcpy(d->dev[v], d->host[v], bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+      return fail("initial upload of %s", vi.name);  // from the pinned copy
+    }
     if (vi.written) {
       if (cudaMalloc(&d->dev_pristine[v], bytes) != cudaSuccess) return fail("pristine alloc for %s", vi.name);
       if (cudaMemcpy(d->dev_pristine[v], d->dev[v], bytes, cudaMemcpyDeviceToDevice) != cudaSuccess)
         return fail("pristine copy of %s", vi.name);
     }
-    memcpy(d->host[v], a->initial[v].data(), bytes);
   }
   d->hv.assign(nv, 1);
   d->dv.assign(nv, 0);
@@ -1184,7 +1191,9 @@ int b2o_app_finalize(uint64_t app) {
   if (a->finalized) return 0;
   for (auto &w : g_rt->workers) {
     AppDev *d = nullptr;
-    if (make_replica(a, w.get(), &d) != 0) return -1;
+    // worker 0 uploads over PCIe, the others copy from it over NVLink
+    const AppDev *src = w->index > 0 ? a->per_worker[0].get() : nullptr;
+    if (make_replica(a, w.get(), &d, src) != 0) return -1;
   }
   a->finalized = true;
   bool need_ref = false;
