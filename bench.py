@@ -139,6 +139,14 @@ class Clocks:
                                          stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+        # nvidia-smi takes a moment to start: the timed region begins once it
+        # is sampling, so the samples cover the region
+        t0 = time.time()
+        while self.proc and time.time() - t0 < 5.0:
+            self.out.flush()
+            if Path(self.out.name).stat().st_size > 0:
+                break
+            time.sleep(0.02)
         return self
 
     def __exit__(self, *exc):
