@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-34"
+COMPILER_VERSION = "b2o-compiler-36"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -1593,6 +1593,8 @@ class _Gen:
             out.append(f"  const int32_t vJ{p_} = j0_ + tx_ * {R} + {p_};")
         out.append(f"  const int32_t klo_ = {self.bound(K.lower, self.local_name)}, "
                    f"khi_ = {self.bound(K.upper, self.local_name)};")
+        out.append(f"  const bool full_ = i0_ + {TI} <= ie_ && j0_ + {TJ} <= je_;")
+        out.append("  (void)full_;")
 
         def sub(e, p_, q_, inner):
             """C text of ``e`` for point (p_, q_) of the micro-tile."""
@@ -1655,31 +1657,46 @@ class _Gen:
         # the current stage is consumed from shared memory
         ELT = BK * max(TI, TJ) // nthr
 
-        def tile_load(side, t, v, co, c0, kb, dst, ind):
+        swz = bool(self.spec.get("ktile_swz", True))
+
+        def slot(cod, ov, ext, r_):
+            """(k, other) tile coordinates of staging element r_ of this
+            thread.  When k has unit stride, lanes walk k; with ``swz`` a warp
+            covers 8 consecutive k of 4 rows (32-byte segments, still whole
+            sectors) so the transposed shared-memory stores hit 32 distinct
+            banks (row pitch ext+4 = 4 mod 32)."""
+            e = f"(threadIdx.x + {r_ * nthr})"
+            kfast = abs(cod.get(kv, 0)) == 1 and abs(cod.get(ov, 0)) != 1
+            if not kfast:
+                return f"({e} / {ext})", f"({e} % {ext})"
+            if swz and BK % 8 == 0 and ext % 4 == 0:
+                return f"(({e} & 7) + 8 * ({e} / {8 * ext}))", f"(({e} >> 3) % {ext})"
+            return f"({e} % {BK})", f"({e} / {BK})"
+
+        def tile_load(side, t, v, co, c0, kb, dst, ind, guard=True):
             cod = dict(co)
             ext = TI if side == "A" else TJ
             ov = iv if side == "A" else jv
             o0, oe = ("i0_", "ie_") if side == "A" else ("j0_", "je_")
-            kfast = abs(cod.get(kv, 0)) == 1 and abs(cod.get(ov, 0)) != 1
             for r_ in range(BK * ext // nthr):
-                e = f"(threadIdx.x + {r_ * nthr})"
-                kk, oo = (f"({e} % {BK})", f"({e} / {BK})") if kfast else (f"({e} / {ext})", f"({e} % {ext})")
+                kk, oo = slot(cod, ov, ext, r_)
                 terms = [f"(int64_t){cod.get(kv, 0)} * ({kb} + {kk})", f"(int64_t){cod.get(ov, 0)} * ({o0} + {oo})"]
                 for x, c in cod.items():
                     if x not in (kv, ov):
                         terms.append(f"(int64_t){c} * {self.local_name(x, False)}")
                 addr = " + ".join(terms + [f"(int64_t){c0}"])
-                out.append(f"{ind}{dst(r_, kk, oo)} = ({kb} + {kk} < khi_ && {o0} + {oo} < {oe}) "
-                           f"? __ldg(v{v} + ({addr})) : 0.f;")
+                if guard:
+                    out.append(f"{ind}{dst(r_, kk, oo)} = ({kb} + {kk} < khi_ && {o0} + {oo} < {oe}) "
+                               f"? __ldg(v{v} + ({addr})) : 0.f;")
+                else:
+                    out.append(f"{ind}{dst(r_, kk, oo)} = __ldg(v{v} + ({addr}));")
 
         def tile_store(side, t, v, co, c0, ind):
             cod = dict(co)
             ext = TI if side == "A" else TJ
             ov = iv if side == "A" else jv
-            kfast = abs(cod.get(kv, 0)) == 1 and abs(cod.get(ov, 0)) != 1
             for r_ in range(BK * ext // nthr):
-                e = f"(threadIdx.x + {r_ * nthr})"
-                kk, oo = (f"({e} % {BK})", f"({e} / {BK})") if kfast else (f"({e} / {ext})", f"({e} % {ext})")
+                kk, oo = slot(cod, ov, ext, r_)
                 out.append(f"{ind}s{t}_[{kk}][{oo}] = p{t}_{r_};")
 
         for (v, co, c0), (side, t) in tiles:
@@ -1693,22 +1710,69 @@ class _Gen:
         out.append("  __syncthreads();")
         out.append(f"  for (int32_t kb_ = klo_; kb_ < khi_; kb_ += {BK}) {{")
         out.append(f"    const int32_t kn_ = min({BK}, khi_ - kb_);")
+        # fast paths (bit-identical: the per-point operation sequence is
+        # unchanged): unguarded staging loads when the whole next stage lies
+        # inside the nest's ranges, and a fully unrolled k stage with the next
+        # k's shared-memory operands loaded one step ahead
+        fast = bool(self.spec.get("ktile_fast", True))
         out.append(f"    if (kb_ + {BK} < khi_) {{")
-        for (v, co, c0), (side, t) in tiles:
-            tile_load(side, t, v, co, c0, f"(kb_ + {BK})", lambda r_, kk, oo, t=t: f"p{t}_{r_}", "      ")
+        if fast:
+            out.append(f"      if (full_ && kb_ + {2 * BK} <= khi_) {{")
+            for (v, co, c0), (side, t) in tiles:
+                tile_load(side, t, v, co, c0, f"(kb_ + {BK})", lambda r_, kk, oo, t=t: f"p{t}_{r_}", "        ",
+                          guard=False)
+            out.append("      } else {")
+            for (v, co, c0), (side, t) in tiles:
+                tile_load(side, t, v, co, c0, f"(kb_ + {BK})", lambda r_, kk, oo, t=t: f"p{t}_{r_}", "        ")
+            out.append("      }")
+        else:
+            for (v, co, c0), (side, t) in tiles:
+                tile_load(side, t, v, co, c0, f"(kb_ + {BK})", lambda r_, kk, oo, t=t: f"p{t}_{r_}", "      ")
         out.append("    }")
+
+        def operands(kk, src, ind):
+            for (v, co, c0), (side, t) in tiles:
+                nm, off = (f"a{t}", "ty_") if side == "A" else (f"b{t}", "tx_")
+                for h_ in range(R // 4):
+                    rhs = (f"*reinterpret_cast<const float4 *>(&s{t}_[{kk}][{off} * {R} + {4 * h_}])"
+                           if src is None else f"{nm}n{h_}_")
+                    out.append(f"{ind}const float4 {nm}q{h_}_ = {rhs};")
+                for p_ in range(R):
+                    out.append(f"{ind}const float {nm}_{p_} = {nm}q{p_ // 4}_.{'xyzw'[p_ % 4]};")
+
+        def prefetch(kk, decl, ind):
+            for (v, co, c0), (side, t) in tiles:
+                nm, off = (f"a{t}", "ty_") if side == "A" else (f"b{t}", "tx_")
+                for h_ in range(R // 4):
+                    out.append(f"{ind}{'float4 ' if decl else ''}{nm}n{h_}_ = "
+                               f"*reinterpret_cast<const float4 *>(&s{t}_[{kk}][{off} * {R} + {4 * h_}]);")
+
+        if fast:
+            pf = bool(self.spec.get("ktile_prefetch", True))
+            out.append(f"    if (kn_ == {BK}) {{")
+            if pf:
+                prefetch("0", True, "      ")
+            out.append("#pragma unroll")
+            out.append(f"      for (int kk_ = 0; kk_ < {BK}; ++kk_) {{")
+            out.append("        const int32_t vK_ = kb_ + kk_;")
+            operands("kk_", "n" if pf else None, "        ")
+            if pf:
+                out.append(f"        if (kk_ + 1 < {BK}) {{")
+                prefetch("kk_ + 1", False, "          ")
+                out.append("        }")
+            emit(kbody, True, "        ")
+            out.append("        (void)vK_;")
+            out.append("      }")
+            out.append("    } else {")
         out.append("#pragma unroll 4")
         out.append("    for (int kk_ = 0; kk_ < kn_; ++kk_) {")
         out.append("      const int32_t vK_ = kb_ + kk_;")
-        for (v, co, c0), (side, t) in tiles:
-            nm, off = (f"a{t}", "ty_") if side == "A" else (f"b{t}", "tx_")
-            for h_ in range(R // 4):
-                out.append(f"      const float4 {nm}q{h_}_ = *reinterpret_cast<const float4 *>(&s{t}_[kk_][{off} * {R} + {4 * h_}]);")
-            for p_ in range(R):
-                out.append(f"      const float {nm}_{p_} = {nm}q{p_ // 4}_.{'xyzw'[p_ % 4]};")
+        operands("kk_", None, "      ")
         emit(kbody, True, "      ")
         out.append("      (void)vK_;")
         out.append("    }")
+        if fast:
+            out.append("    }")
         out.append(f"    if (kb_ + {BK} < khi_) {{")
         out.append("      __syncthreads();")
         for (v, co, c0), (side, t) in tiles:
@@ -2117,7 +2181,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "progressive_d2h", "exact_reductions", "ktile_tile", "ktile_r", "reductions")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "progressive_d2h", "exact_reductions", "ktile_tile", "ktile_r", "ktile_fast", "ktile_prefetch", "ktile_swz", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:
