@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-36"
+COMPILER_VERSION = "b2o-compiler-38"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -1478,6 +1478,26 @@ class _Gen:
             out.append(f"    {vt} {cname(v, d, o)} = {ldexpr(v, d, o)};")
         carried = {k for k in keys if (k[0], k[1] + 1, k[2]) in keys and k[0] not in qp["writes"]}
         lead = sorted(keys - carried)
+        # staged leading plane: each thread copies its own next-plane chunks
+        # into private shared-memory slots (cp.async, P-stage ring) and reads
+        # them back one step later -- no barrier (a thread reads only what it
+        # copied), the copies in flight hold no registers
+        P = int(self.spec.get("march_async", 0) or 0)
+        staged = [k for k in lead if k[0] not in qp["writes"]] if P >= 2 else []
+        if staged:
+            vts = {self.T(v) for v, _, _ in staged}
+            if vts - {"float", "int32_t"}:
+                staged = []
+        if staged:
+            NS = len(staged)
+            out.append(f"    __shared__ __align__(16) int4 st_[{P}][{NS}][{bt}];")
+            sidx = {k: i for i, k in enumerate(staged)}
+
+            def issue(plane_off, slot, ind):
+                for i, (v, d, o) in enumerate(staged):
+                    off = (d + plane_off) * C0 // QUAD + o
+                    out.append(f"{ind}b2o_cp16(&st_[{slot}][{i}][threadIdx.x], "
+                               f"reinterpret_cast<const int4 *>(v{v} + b_) + ({off}));")
         # software pipelining: the chunks the next plane loads are issued
         # before this plane's arithmetic (prefetch registers n*)
         pipe = bool(self.spec.get("march_prefetch", False))  # measured slower
@@ -1485,14 +1505,33 @@ class _Gen:
             for v, d, o in lead:
                 vt = "float4" if self.T(v) == "float" else "int4"
                 out.append(f"    {vt} n{cname(v, d, o)};")
+        if staged:
+            # prologue: planes 1 .. P-1 into slots 1 .. P-1 (one group each)
+            for q in range(1, P):
+                out.append(f"    if ({q}u < zn_) {{")
+                issue(q, q, "      ")
+                out.append("    }")
+                out.append("    b2o_cp_commit();")
         out.append("    for (uint32_t s_ = 0; s_ < zn_; ++s_) {")
         out.append("      if (s_ > 0) {")
         out.append(f"        b_ += (int64_t){C0}; ++v{iv[0]};")
+        if staged:
+            # plane s_+P-1 goes out, plane s_ must be in: P-1 younger groups
+            # may stay pending
+            out.append(f"        if (s_ + {P - 1}u < zn_) {{")
+            issue(P - 1, f"(s_ + {P - 1}u) % {P}u", "          ")
+            out.append("        }")
+            out.append("        b2o_cp_commit();")
+            out.append(f"        b2o_cp_wait<{P - 1}>();")
         # ascending plane offset: the old value of (d+1) is read before it
         # is replaced
         for v, d, o in sorted(keys, key=lambda k: (k[1], k[0], k[2])):
             if (v, d, o) in carried:
                 out.append(f"        {cname(v, d, o)} = {cname(v, d + 1, o)};")
+            elif staged and (v, d, o) in sidx:
+                vt = "float4" if self.T(v) == "float" else "int4"
+                out.append(f"        {cname(v, d, o)} = *reinterpret_cast<const {vt} *>("
+                           f"&st_[s_ % {P}u][{sidx[(v, d, o)]}][threadIdx.x]);")
             elif pipe:
                 out.append(f"        {cname(v, d, o)} = n{cname(v, d, o)};")
             else:
@@ -2181,7 +2220,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "ktile", "progressive_d2h", "exact_reductions", "ktile_tile", "ktile_r", "ktile_fast", "ktile_prefetch", "ktile_swz", "reductions")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "march_async", "ktile", "progressive_d2h", "exact_reductions", "ktile_tile", "ktile_r", "ktile_fast", "ktile_prefetch", "ktile_swz", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

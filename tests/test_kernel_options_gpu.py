@@ -3,7 +3,7 @@ DESIGN.md §4) stay correct: every genome of a few apps and fuzz programs,
 compiled with each option, leaves the C oracle's final state bit for bit
 (spec["stencil"] 2.5-D smem template, spec["brick"]-style k-blocking,
 points per thread, two quads per thread, warp-shuffle neighbour exchange,
-march prefetch, march / k-tile / progressive downloads switched off)."""
+march prefetch, cp.async-staged march planes, k-tile stage fast path off, march / k-tile / progressive downloads switched off)."""
 
 import copy
 import json
@@ -25,6 +25,11 @@ OPTIONS = [
     {"march_prefetch": True},
     {"quad_march": 0},
     {"quad_march": 4, "march_block": 64},
+    {"march_async": 2},
+    {"march_async": 3, "march_block": 64},
+    {"march_async": 2, "quad_march": 16},
+    {"ktile_fast": False},
+    {"ktile_prefetch": False, "ktile_swz": False},
     {"ktile": False},
     {"ktile_tile": 32},
     {"ktile_r": 8},
