@@ -91,3 +91,43 @@ def test_fastdiv_exact():
     for d in ds:
         for n in ns:
             assert _fastdiv(n, d) == n // d, (n, d)
+
+
+def _c_int(expr: str, tid: int) -> int:
+    """Evaluate a generated non-negative C integer index expression."""
+    py = expr.replace("threadIdx.x", str(tid)).replace("/", "//")
+    return eval(py, {})  # noqa: S307 -- generated arithmetic on literals only
+
+
+@pytest.mark.parametrize("opts", [{}, {"ktile_swz": False}])
+def test_ktile_staging_covers_each_tile_element_once(opts):
+    """The k-tile kernel's shared-memory staging map (matmul 1024, i-root):
+    over all threads and stage slots every (k, row) element of each operand
+    tile is stored exactly once; with the default swizzle every warp's
+    transposed stores of the k-contiguous operand hit 32 distinct banks."""
+    import re
+
+    g = golden("matmul_1024")
+    dev = generate_sources(g["doc"], dict(g["spec"], **opts))[1]
+    body = dev[dev.find("b2o_k0("):]
+    body = body[:body.find("__syncthreads();")]  # the prologue stores
+    decl = dict((int(t), (int(bk), int(ext))) for t, bk, ext in
+                re.findall(r"__shared__ __align__\(16\) float s(\d+)_\[(\d+)\]\[(\d+)\];", dev))
+    stores = re.findall(r"\n  s(\d+)_\[(.+?)\]\[(.+?)\] = p\d+_(\d+);", body)
+    assert stores and decl
+    nthr = 256
+    for t, (bk, pitch) in decl.items():
+        mine = [(kk, oo) for tt, kk, oo, _ in stores if int(tt) == t]
+        seen = {}
+        for kk, oo in mine:
+            for tid in range(nthr):
+                key = (_c_int(kk, tid), _c_int(oo, tid))
+                seen[key] = seen.get(key, 0) + 1
+        ext = pitch - 4
+        assert set(seen) == {(k, o) for k in range(bk) for o in range(ext)}, t
+        assert set(seen.values()) == {1}, t
+        if not opts and t == 0:  # A(i, k): k has unit stride -> transposed stores
+            for kk, oo in mine:
+                for w in range(nthr // 32):
+                    banks = {(_c_int(kk, tid) * pitch + _c_int(oo, tid)) % 32 for tid in range(32 * w, 32 * w + 32)}
+                    assert len(banks) == 32, (kk, oo, w, len(banks))
