@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-38"
+COMPILER_VERSION = "b2o-compiler-39"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -1012,8 +1012,9 @@ class _Gen:
         if n.shape == "ktile":
             T = int(self.spec.get("ktile_tile", KT_TI))
             R = int(self.spec.get("ktile_r", KT_R))
+            RI = int(self.spec.get("ktile_ri", R))
             out.append(f"  geom[0] = (a.n[1] + {T - 1}) / {T}; geom[1] = (a.n[0] + {T - 1}) / {T}; "
-                       f"geom[2] = 1; geom[3] = {T * T // (R * R)}; geom[4] = geom[5] = 1;")
+                       f"geom[2] = 1; geom[3] = {T * T // (RI * R)}; geom[4] = geom[5] = 1;")
         elif n.shape == "brick":
             tk, tj = STENCIL_TILE
             out.append(f"  geom[0] = (a.n[2] + {tk - 1}) / {tk}; geom[1] = (a.n[1] + {tj - 1}) / {tj}; "
@@ -1608,7 +1609,8 @@ class _Gen:
         iv, jv, kv = kp["iv"], kp["jv"], kp["kv"]
         T = int(self.spec.get("ktile_tile", KT_TI))
         R, TI, TJ, BK = int(self.spec.get("ktile_r", KT_R)), T, T, KT_BK
-        nthr = TI * TJ // (R * R)
+        RI = int(self.spec.get("ktile_ri", R))  # micro-tile rows (i); R columns (j)
+        nthr = TI * TJ // (RI * R)
         TX = TJ // R  # threads along j
         K = prog.loops[kp["kloop"]]
         body = prog.regions[prog.loops[n.chain[1]].body].statements
@@ -1627,9 +1629,10 @@ class _Gen:
         out.append(f"  const int32_t i0_ = a.lo[0] + (int32_t)(blockIdx.y * {TI}u), "
                    f"j0_ = a.lo[1] + (int32_t)(blockIdx.x * {TJ}u);")
         out.append(f"  const int32_t ie_ = a.lo[0] + (int32_t)a.n[0], je_ = a.lo[1] + (int32_t)a.n[1];")
-        for p_ in range(R):
-            out.append(f"  const int32_t vI{p_} = i0_ + ty_ * {R} + {p_};")
-            out.append(f"  const int32_t vJ{p_} = j0_ + tx_ * {R} + {p_};")
+        for p_ in range(RI):
+            out.append(f"  const int32_t vI{p_} = i0_ + ty_ * {RI} + {p_};")
+        for q_ in range(R):
+            out.append(f"  const int32_t vJ{q_} = j0_ + tx_ * {R} + {q_};")
         out.append(f"  const int32_t klo_ = {self.bound(K.lower, self.local_name)}, "
                    f"khi_ = {self.bound(K.upper, self.local_name)};")
         out.append(f"  const bool full_ = i0_ + {TI} <= ie_ && j0_ + {TJ} <= je_;")
@@ -1669,7 +1672,7 @@ class _Gen:
                     first_read.setdefault(r[1], True)
             first_read.setdefault(st.target[1], False)
         for v in sorted(kp["accs"]):
-            for p_ in range(R):
+            for p_ in range(RI):
                 for q_ in range(R):
                     if first_read.get(v):
                         # the accumulator starts from the array's current value
@@ -1681,7 +1684,7 @@ class _Gen:
         def emit(sts, inner, ind):
             for st in sts:
                 v = st.target[1]
-                for p_ in range(R):
+                for p_ in range(RI):
                     for q_ in range(R):
                         val = sub(st.value, p_, q_, inner)
                         line = f"acc{v}_{p_}{q_} = (float)({val});"
@@ -1772,19 +1775,21 @@ class _Gen:
         def operands(kk, src, ind):
             for (v, co, c0), (side, t) in tiles:
                 nm, off = (f"a{t}", "ty_") if side == "A" else (f"b{t}", "tx_")
-                for h_ in range(R // 4):
-                    rhs = (f"*reinterpret_cast<const float4 *>(&s{t}_[{kk}][{off} * {R} + {4 * h_}])"
+                RS = RI if side == "A" else R
+                for h_ in range(RS // 4):
+                    rhs = (f"*reinterpret_cast<const float4 *>(&s{t}_[{kk}][{off} * {RS} + {4 * h_}])"
                            if src is None else f"{nm}n{h_}_")
                     out.append(f"{ind}const float4 {nm}q{h_}_ = {rhs};")
-                for p_ in range(R):
+                for p_ in range(RS):
                     out.append(f"{ind}const float {nm}_{p_} = {nm}q{p_ // 4}_.{'xyzw'[p_ % 4]};")
 
         def prefetch(kk, decl, ind):
             for (v, co, c0), (side, t) in tiles:
                 nm, off = (f"a{t}", "ty_") if side == "A" else (f"b{t}", "tx_")
-                for h_ in range(R // 4):
+                RS = RI if side == "A" else R
+                for h_ in range(RS // 4):
                     out.append(f"{ind}{'float4 ' if decl else ''}{nm}n{h_}_ = "
-                               f"*reinterpret_cast<const float4 *>(&s{t}_[{kk}][{off} * {R} + {4 * h_}]);")
+                               f"*reinterpret_cast<const float4 *>(&s{t}_[{kk}][{off} * {RS} + {4 * h_}]);")
 
         if fast:
             pf = bool(self.spec.get("ktile_prefetch", True))
@@ -1822,7 +1827,7 @@ class _Gen:
         emit(post, False, "  ")
         out.append("  b2o_pdl_trigger();")
         for v in sorted(kp["accs"]):
-            for p_ in range(R):
+            for p_ in range(RI):
                 for q_ in range(R):
                     idx = sub(self._acc_index(kp, v), p_, q_, False)
                     out.append(f"  if (vI{p_} < ie_ && vJ{q_} < je_) v{v}[{idx}] = acc{v}_{p_}{q_};")
@@ -2220,7 +2225,7 @@ class CompiledApp:
 def _spec_key(spec: dict) -> dict:
     return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
                                      "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "march_async", "ktile", "progressive_d2h", "exact_reductions", "ktile_tile", "ktile_r", "ktile_fast", "ktile_prefetch", "ktile_swz", "reductions")}
+                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "march_async", "ktile", "progressive_d2h", "exact_reductions", "ktile_tile", "ktile_r", "ktile_ri", "ktile_fast", "ktile_prefetch", "ktile_swz", "reductions")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

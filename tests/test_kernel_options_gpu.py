@@ -29,6 +29,7 @@ OPTIONS = [
     {"march_async": 3, "march_block": 64},
     {"march_async": 2, "quad_march": 16},
     {"ktile_fast": False},
+    {"ktile_ri": 8},
     {"ktile_prefetch": False, "ktile_swz": False},
     {"ktile": False},
     {"ktile_tile": 32},

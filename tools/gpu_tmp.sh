@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-CS=/usr/local/cuda/bin/compute-sanitizer
-timeout 1200 $CS --tool racecheck --print-limit 20 python tools/san_ktile.py > gpurun_out/san_racecheck_ktile_s4.log 2>&1
-timeout 900 $CS --tool memcheck --print-limit 20 python tools/san_ktile.py > gpurun_out/san_memcheck_ktile_s4.log 2>&1
-true
+timeout 600 python tools/kernel_sweep.py matmul_1024 10 '{}' '{"ktile_ri":8}' '{}' '{"ktile_ri":8}' > gpurun_out/sweep_mm5.log 2>&1
+timeout 900 python -m pytest tests/test_kernel_options_gpu.py -m gpu -q -x -k "ktile" > gpurun_out/pytest_q.log 2>&1
