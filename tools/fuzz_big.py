@@ -1,9 +1,10 @@
 """One-off large differential fuzz (not part of the committed suite).
 
   build  (here, with the reference importable):
-      PYTHONPATH=/root/reference/pkg/src python tools/fuzz_big.py build N
+      PYTHONPATH=/root/reference/pkg/src python tools/fuzz_big.py build N [BASE]
       -> tools/_bigfuzz.json: N general + N shape programs with the
-         reference's plans for up to 64 genomes each
+         reference's plans for up to 64 genomes each (general seeds from
+         BASE, shape seeds from BASE + 1000; default 5000)
   run    (on a B200):   python tools/fuzz_big.py run [fp32|fp64]
       -> every genome vs the C oracle, bit for bit; prints a summary line
 """
@@ -18,7 +19,7 @@ sys.path.insert(0, str(ROOT / "tests"))
 OUT = ROOT / "tools" / "_bigfuzz.json"
 
 
-def build(n: int) -> None:
+def build(n: int, base: int = 5000) -> None:
     sys.path.insert(0, str(ROOT / "tests" / "golden"))
     sys.argv = ["make_golden.py"]
     import make_golden as mg
@@ -30,10 +31,10 @@ def build(n: int) -> None:
     from paper_2011_03602_b200.reductions import screen_model_with_reductions
 
     rec = {}
-    for seed in range(5000, 5000 + n):
+    for seed in range(base, base + n):
         m = parse_mini_source(_fuzz.program(seed))
         rec[f"g{seed}"] = mg.app_record(f"g{seed}", m, _fuzz.spec(seed), all_genomes_cap=64)
-    for seed in range(6000, 6000 + n):
+    for seed in range(base + 1000, base + 1000 + n):
         m = parse_mini_source(_fuzz_shapes.program(seed))
         sp = _fuzz_shapes.spec(seed)
         scr = screen_model_with_reductions if sp.get("reductions") else screen_model
@@ -81,6 +82,6 @@ def run(precision: str = "fp32") -> None:
 
 if __name__ == "__main__":
     if sys.argv[1] == "build":
-        build(int(sys.argv[2]))
+        build(int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 5000)
     else:
         run(sys.argv[2] if len(sys.argv) > 2 else "fp32")
