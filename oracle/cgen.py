@@ -8,6 +8,9 @@ the C semantics the reference implies (see ``oracle/interp.py`` for the
 ledger; the C text mirrors the ``c_openacc`` rendering, ``src/codegen.py:57-68``
 and ``:189-200``).  It is pinned against ``oracle/interp.py`` on the small
 fixtures and against closed forms (numpy matmul, a direct Himeno formula).
+No reference test executes a program, so numeric app outputs are "parity
+unpinned" by the reference; what the reference does pin
+(placements, plans, screen verdicts) comes from the reference itself.
 
 ``openmp=True`` adds ``#pragma omp parallel for`` to the outermost loops that
 pass the reference's parallelizability screen (restated from
