@@ -94,4 +94,4 @@ def spec(seed: int) -> dict:
     }
 
 
-SEEDS = list(range(48))
+SEEDS = list(range(96))
