@@ -23,7 +23,7 @@ from __future__ import annotations
 
 import random
 
-SEEDS = list(range(54))  # 12 per original family, 6 per second-generation family
+SEEDS = list(range(90))  # 12 per original family, 18 per second-generation family
 
 
 def family(seed: int) -> str:
