@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_fuzz_shapes.py -m gpu -q -x > gpurun_out/pytest_shapes90.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke3.log 2>&1
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_fuzz.py -m gpu -q -x > gpurun_out/pytest_final_q.log 2>&1
