@@ -80,8 +80,13 @@ typedef struct {
   int32_t device;            /* worker index, -1 = any */
   int32_t mode;              /* B2O_MODE_* */
   int32_t repeats;           /* timed runs; time_s is the minimum (>= 1) */
-  int32_t flags;             /* bit0: keep final state readable via b2o_app_read */
+  int32_t flags;             /* B2O_FLAG_* */
 } b2o_pattern;
+
+/* b2o_pattern.flags: the timed run starts with every array's (pristine)
+ * contents already valid in HBM, so the plan's input uploads are elided --
+ * the "inputs resident" step of bench.py's value (e2e runs without it). */
+#define B2O_FLAG_INPUTS_RESIDENT 2
 
 typedef struct {
   double time_s;             /* wall time of the whole program run (valid only) */
@@ -107,6 +112,13 @@ int b2o_shutdown(void);
 const char *b2o_last_error(void);
 int b2o_num_workers(void);
 int b2o_abi_version(void);
+/* Broken-worker recovery: after a sticky CUDA error the faulting job returns
+ * B2O_RUNTIME_ERROR and the runtime resets that device and rebuilds every
+ * app replica on it before the next job (b2o_runtime.cu recover_device).
+ * b2o_worker_recoveries counts those resets; b2o_debug_inject_fault makes the
+ * worker's next job trap on the device (tests only). */
+int b2o_debug_inject_fault(int32_t worker);
+int64_t b2o_worker_recoveries(int32_t worker);
 
 /* app = one compiled program (host module + cubin from compiler.py) */
 int b2o_app_create(const char *host_module, const char *cubin, uint64_t *app);

@@ -259,6 +259,16 @@ class CProgram:
                 s = stmts[rid][idx]
                 binder("replaced", {"name": s["replaced"], "args": s["args"], "rid": rid, "index": idx}, st)
 
-        cb = EXT_FN(ext)
+        errors: list[BaseException] = []
+
+        def guarded(kind, ident, _slots):
+            try:
+                ext(kind, ident, _slots)
+            except BaseException as exc:  # noqa: BLE001 -- ctypes would swallow it
+                errors.append(exc)
+
+        cb = EXT_FN(guarded)
         self.fn(slots, cb)
+        if errors:
+            raise RuntimeError(f"external call failed inside the oracle program: {errors[0]!r}") from errors[0]
         return st

@@ -5,8 +5,10 @@ the ``matmul``/``fft`` records of ``fixtures/sample_db.json`` and replaces by
 
 CPU semantics of the original calls: ``gemm(A, B, C)``
 is C = A B (n x n, row-major); ``fft(x, y)`` is y = FFT2(x), interleaved
-complex ``float[2 n^2]``.  Outputs are compared norm-wise (documented
-deviation).
+complex ``float[2 n^2]``.  ``mc`` is compared element-wise (the reference
+rule, src/evaluators.py:129-139); ``y`` norm-wise (documented deviation,
+SURVEY.md Appendix A.8: FFT outputs near zero have no meaningful relative
+error).
 """
 
 from __future__ import annotations
@@ -30,7 +32,7 @@ def spec(n_gemm: int = 4096, n_fft: int = 4096, seed: int = 20240817) -> dict:
             "x": {"kind": "uniform", "seed": seed + 2, "lo": -1.0, "hi": 1.0},
         },
         "outputs": {
-            "mc": {"rel_tol": 1e-5, "compare": "normwise"},
+            "mc": {"rel_tol": 1e-5},  # element-wise, the reference rule (3xTF32: 1.5e-6 at 4096^3)
             "y": {"rel_tol": 1e-5, "compare": "normwise"},
         },
         "externals": {"gemm": {"kind": "gemm", "out": 2}, "fft": {"kind": "fft2d", "out": 1}},

@@ -25,6 +25,11 @@ import numpy as np
 
 from .ir import Program
 
+# per-precision default of an output's rel_tol when the spec names none.  The
+# reference's validate_output default is 1e-6 (src/evaluators.py:129-139,
+# a harness for doubles printed as text); fp32 apps default to 1e-5 (SURVEY.md
+# Appendix A.8: the reference's own C text computes them in float), a
+# documented deviation.  Every golden app spells its tolerance out.
 DEFAULT_REL_TOL = {"fp32": 1e-5, "fp64": 1e-12}
 
 
@@ -120,7 +125,18 @@ def block_binding(prog: Program, spec: dict, stmt) -> dict:
         out = args[int(desc.get("out", len(args) - 1))]
     ins = [a for a in args if a != out]
     binding = {"kind": kind, "out": out, "ins": ins}
+    _shape(prog, binding, desc)
+    return binding
+
+
+def _shape(prog: Program, binding: dict, desc: dict) -> None:
+    """Operand shapes of a gemm / fft2d / histogram binding, checked against
+    the operand lengths (a mismatch is a ValueError, which the compiler
+    reports as compile_error: never an out-of-bounds library call)."""
+    kind, out, ins = binding["kind"], binding["out"], binding["ins"]
     if kind == "gemm":
+        if len(ins) < 2:
+            raise ValueError("gemm needs two input operands")
         a, b = ins[0], ins[1]
         la, lb, lc = (prog.vars[x].length for x in (a, b, out))
         if "m" in desc:
@@ -128,19 +144,21 @@ def block_binding(prog: Program, spec: dict, stmt) -> dict:
         else:
             n = math.isqrt(lc)
             m, k = n, n
-        if m * k != la or k * n != lb or m * n != lc:
+        if min(m, n, k) <= 0 or m * k != la or k * n != lb or m * n != lc:
             raise ValueError(f"gemm shape {m}x{n}x{k} does not match operand lengths {la},{lb},{lc}")
         binding.update(m=m, n=n, k=k)
     elif kind == "fft2d":
-        x = ins[0]
-        lx = prog.vars[x].length
+        if not ins:
+            raise ValueError("fft2d needs an input operand")
+        lx = prog.vars[ins[0]].length
         n = int(desc.get("n", math.isqrt(lx // 2)))
-        if 2 * n * n != lx or prog.vars[out].length != lx:
+        if n <= 0 or 2 * n * n != lx or prog.vars[out].length != lx:
             raise ValueError(f"fft2d size {n} does not match operand lengths")
         binding.update(n=n)
     elif kind == "histogram":
         _histogram_shape(prog, binding)
-    return binding
+    else:
+        raise ValueError(f"unknown external kind {kind!r}")
 
 
 def _histogram_shape(prog: Program, binding: dict) -> None:
@@ -164,13 +182,5 @@ def external_call_binding(prog: Program, spec: dict, call) -> dict:
     out = args[int(desc.get("out", len(args) - 1))]
     ins = [a for a in args if a != out]
     binding = {"kind": desc["kind"], "out": out, "ins": ins}
-    if desc["kind"] == "gemm":
-        n = math.isqrt(prog.vars[out].length)
-        binding.update(m=int(desc.get("m", n)), n=int(desc.get("n", n)), k=int(desc.get("k", n)))
-    elif desc["kind"] == "fft2d":
-        binding.update(n=int(desc.get("n", math.isqrt(prog.vars[ins[0]].length // 2))))
-    elif desc["kind"] == "histogram":
-        _histogram_shape(prog, binding)
-    else:
-        raise ValueError(f"unknown external kind {desc['kind']!r}")
+    _shape(prog, binding, desc)  # the same length checks as a replaced block
     return binding

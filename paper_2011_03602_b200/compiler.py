@@ -786,9 +786,16 @@ class _Gen:
                 _array_refs(st.init, rs)
                 for r in rs:
                     refs.setdefault(r[1], []).append(r[2])
+        # the generated for-header evaluates the outer bounds before the first
+        # host_wait (and the upper bound every iteration): an array read there
+        # must be complete before the loop starts
+        in_header: list = []
+        _array_refs(prog.loops[lid].lower, in_header)
+        _array_refs(prog.loops[lid].upper, in_header)
+        header_arrays = {r[1] for r in in_header}
         out = {}
         for v, idxs in refs.items():
-            if v in writes or not prog.vars[v].is_array:
+            if v in writes or not prog.vars[v].is_array or v in header_arrays:
                 continue
             C, K = None, None
             for e in idxs:

@@ -685,6 +685,7 @@ struct Workspace {
 };
 std::mutex ws_mu;
 std::map<int, Workspace> ws_by_dev;
+std::atomic<bool> g_pattr[64], g_attr[64];  // per-device smem attribute set (cleared on device reset)
 
 float *workspace(size_t bytes) {
   int dev = 0;
@@ -740,7 +741,7 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
     if (!make_map(&mAh, Ah, (int)m, (int)k, pair::BM) || !make_map(&mAl, Al, (int)m, (int)k, pair::BM) ||
         !make_map(&mBh, Bh, (int)n, (int)k, pair::BNH) || !make_map(&mBl, Bl, (int)n, (int)k, pair::BNH))
       return -1;
-    static std::atomic<bool> pattr[64];  // per device; set once, racing setters are idempotent
+    std::atomic<bool> *pattr = g_pattr;  // per device; set once, racing setters are idempotent
     if (!pattr[dev & 63]) {
       if (cudaFuncSetAttribute(pair::gemm_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                pair::SMEM_BYTES) != cudaSuccess)
@@ -790,7 +791,7 @@ extern "C" int b2o_gemm_tc_f32(const float *A, const float *B, float *C, int64_t
   if (!make_map(&mAh, Ah, (int)m, (int)k, BM) || !make_map(&mAl, Al, (int)m, (int)k, BM) ||
       !make_map(&mBh, Bh, (int)n, (int)k, BN) || !make_map(&mBl, Bl, (int)n, (int)k, BN))
     return -1;
-  static std::atomic<bool> attr[64];
+  std::atomic<bool> *attr = g_attr;
   if (!attr[dev & 63]) {
     if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
       return -1;
@@ -822,6 +823,15 @@ extern "C" int b2o_gemm_f32_phases(const float *A, const float *B, float *C, int
   }
   for (auto &e : ev) cudaEventDestroy(e);
   return rc;
+}
+
+// the device was reset (runtime broken-worker recovery): drop its workspace
+// (freed with the context) and attribute flags
+extern "C" void b2o_gemm_tc_forget_device(int dev) {
+  std::lock_guard<std::mutex> lk(ws_mu);
+  ws_by_dev.erase(dev);
+  g_pattr[dev & 63] = false;
+  g_attr[dev & 63] = false;
 }
 
 // force-load this file's kernels (lazy module loading would otherwise charge

@@ -573,6 +573,9 @@ cudaError_t launch_cols_cluster(float2 *y, const float2 *tw, cudaStream_t s) {
 
 std::mutex tw_mu;
 std::map<std::pair<int, int64_t>, float2 *> tw_cache;  // (device, n) -> table
+// per-device "dynamic shared memory attribute set" flags (cleared when the
+// runtime resets a device, b2o_ops_forget_device)
+std::atomic<bool> g_attr16[64], g_attr_set[64];
 
 float2 *twiddles(int64_t n, bool full = false) {
   int dev = 0;
@@ -603,7 +606,7 @@ extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) 
     float2 *tw = twiddles(n, true);
     if (!tw) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-    static std::atomic<bool> attr16[64];
+    std::atomic<bool> *attr16 = g_attr16;
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr16[dev & 63]) {
@@ -647,7 +650,7 @@ extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) 
   cudaStream_t s = (cudaStream_t)stream;
   size_t row_smem = sizeof(float2) * n;
   size_t col_smem = sizeof(float2) * n * kColGroup;
-  static std::atomic<bool> attr_set[64];
+  std::atomic<bool> *attr_set = g_attr_set;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
@@ -658,6 +661,18 @@ extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) 
   fft_rows_kernel<<<(unsigned)n, kFftThreads, row_smem, s>>>((const float2 *)x, (float2 *)y, (int)n, logn, tw);
   fft_cols_kernel<<<(unsigned)(n / kColGroup), kFftThreads, col_smem, s>>>((float2 *)y, (int)n, logn, tw);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// the device was reset (runtime broken-worker recovery): its twiddle tables
+// and function attributes are gone with the context
+extern "C" void b2o_ops_forget_device(int dev) {
+  std::lock_guard<std::mutex> lk(tw_mu);
+  for (auto it = tw_cache.begin(); it != tw_cache.end();) {
+    if (it->first.first == dev) it = tw_cache.erase(it);
+    else ++it;
+  }
+  g_attr16[dev & 63] = false;
+  g_attr_set[dev & 63] = false;
 }
 
 // force-load this file's kernels (lazy module loading would otherwise charge

@@ -20,6 +20,11 @@ void b2o_ops_warm(void);
 void b2o_gemm_tc_warm(void);
 void b2o_gemm_warm(void);
 void b2o_xsum_warm(void);
+// forget per-device caches (device allocations, function attributes) after
+// the runtime reset that device (broken-worker recovery)
+void b2o_ops_forget_device(int dev);
+void b2o_gemm_tc_forget_device(int dev);
+void b2o_xsum_forget_device(int dev);
 
 #ifdef __cplusplus
 }

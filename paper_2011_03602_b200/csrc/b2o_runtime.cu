@@ -34,6 +34,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <thread>
 #include <vector>
@@ -71,8 +72,10 @@ struct Worker {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::thread th;
-  bool broken = false;
+  bool broken = false;        // a sticky CUDA error killed this device's context
   std::string broken_why;
+  std::atomic<int> inject_fault{0};  // test hook: trap before the next job's run
+  uint64_t recoveries = 0;    // device resets performed after a sticky error
   std::atomic<int64_t> deadline_ns{0};
   std::atomic<b2o_exec *> running{nullptr};
   std::atomic<int> timed_out{0};
@@ -163,6 +166,10 @@ struct Runtime {
   std::map<uint64_t, std::unique_ptr<AppShared>> apps;
   std::map<uint64_t, std::unique_ptr<Batch>> batches;
   uint64_t next_id = 1;
+  // broken-worker recovery (under qmu): jobs executing per device, and the
+  // devices whose workers must not start new jobs while one is being reset
+  std::map<int, int> active;
+  std::set<int> paused;
 };
 
 Runtime *g_rt = nullptr;
@@ -749,6 +756,36 @@ int make_replica(AppShared *a, Worker *w, AppDev **out, const AppDev *src = null
   return 0;
 }
 
+// release every resource of one replica (device and pinned host memory,
+// the loaded cubin); the caller has selected the device and drained the stream
+void free_app_dev(AppShared *a, AppDev *d) {
+  for (void *p : d->dev_alloc) if (p) cudaFree(p);
+  for (void *p : d->dev_pristine) if (p) cudaFree(p);
+  for (size_t v = 0; v < d->host.size(); ++v)
+    if (a->info->vars[v].is_array && d->host[v]) cudaFreeHost(d->host[v]);
+  if (d->cells) cudaFreeHost(d->cells);
+  if (d->slab_init) cudaFreeHost(d->slab_init);
+  if (d->slab) cudaFree(d->slab);
+  if (d->scratch) cudaFree(d->scratch);
+  for (void *p : d->red_bufs) if (p) cudaFree(p);
+  if (d->xsum_ws) cudaFree(d->xsum_ws);
+  if (d->mod) drv.moduleUnload(d->mod);
+  for (auto &p : d->pend)
+    for (cudaEvent_t e : p.ev) cudaEventDestroy(e);
+  d->pend.clear();
+  d->dev_alloc.clear();
+  d->dev_pristine.clear();
+  d->host.clear();
+  d->red_bufs.clear();
+  d->cells = nullptr;
+  d->slab_init = nullptr;
+  d->slab = nullptr;
+  d->scratch = nullptr;
+  d->xsum_ws = nullptr;
+  d->xsum_ws_bytes = 0;
+  d->mod = nullptr;
+}
+
 void par_memcpy(void *dst, const void *src, size_t bytes) {
   if (bytes < ((size_t)16 << 20)) {
     memcpy(dst, src, bytes);
@@ -770,8 +807,13 @@ void reset_state(AppDev *d) {
     const b2o_var_info &vi = info->vars[v];
     if (!vi.is_array) {
       memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
-    } else if (vi.written && d->host_touched[v]) {
-      par_memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
+    } else if (vi.written) {
+      if (d->host_touched[v]) par_memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
+      // a device copy a kernel or an upload changed is restored whether or
+      // not the host ever saw it: prepare_dev_write treats an array the host
+      // did not modify since reset as present-by-allocation (pristine), so a
+      // written-but-never-downloaded intermediate must not keep the previous
+      // job's values
       if (d->dev_dirty[v])
         cudaMemcpyAsync(d->dev[v], d->dev_pristine[v], d->app->initial[v].size(), cudaMemcpyDeviceToDevice,
                         d->w->stream);
@@ -902,6 +944,9 @@ void compare_outputs(AppDev *d, b2o_result &r) {
   }
 }
 
+// test hook target (b2o_debug_inject_fault): a sticky launch failure
+__global__ void b2o_trap_kernel() { asm volatile("trap;"); }
+
 void execute(Worker *w, Job &j) {
   b2o_result &r = j.res;
   r = b2o_result{};
@@ -935,11 +980,15 @@ void execute(Worker *w, Job &j) {
     auto tr = Clock::now();
     nvtxRangePushA("b2o:reset");
     reset_state(d);
+    if (j.pat.flags & B2O_FLAG_INPUTS_RESIDENT)
+      for (int v = 0; v < j.app->info->n_vars; ++v)
+        if (VI(d, v).is_array) d->dv[v] = 1;  // pristine on both sides after the reset
     nvtxRangePop();
     reset_ms += std::chrono::duration<double, std::milli>(Clock::now() - tr).count();
     w->timed_out = 0;
     w->deadline_ns = j.pat.timeout_s > 0 ? now_ns() + (int64_t)(j.pat.timeout_s * 1e9) : 0;
     w->running = &d->ex;
+    if (w->inject_fault.exchange(0)) b2o_trap_kernel<<<1, 1, 0, w->stream>>>();
     auto t0 = Clock::now();
     nvtxRangePushA("b2o:pattern");  // the timed program run
     j.app->run(&d->ex);
@@ -1001,6 +1050,84 @@ void execute(Worker *w, Job &j) {
   }
 }
 
+// Broken-worker recovery.  A sticky CUDA error (illegal address, trap, ...)
+// leaves the device's context unusable: the faulting job came back
+// runtime_error, and without recovery every later job on the device would
+// too.  The first broken worker of the device pauses the device (no new job
+// starts on it), waits for the jobs still running there to finish (they fail
+// fast on the dead context), resets the device, recreates the workers'
+// streams and every app's replica on it from the host copy of the initial
+// state, and resumes the queue.  Jobs running on a sibling worker of the same
+// device at the moment of the fault return runtime_error; queued jobs run
+// after the reset.  cudaDeviceReset destroys the primary context, so device
+// memory another library allocated in this process on that device (e.g.
+// torch tensors) is lost too.
+void recover_device(Worker *w) {
+  const int dev = w->device;
+  {
+    std::unique_lock<std::mutex> lk(g_rt->qmu);
+    if (!w->broken) return;
+    if (g_rt->paused.count(dev)) {  // a sibling worker is resetting the device
+      g_rt->qcv.wait(lk, [&] { return g_rt->stopping || !g_rt->paused.count(dev); });
+      return;
+    }
+    g_rt->paused.insert(dev);
+    g_rt->qcv.wait(lk, [&] { return g_rt->active[dev] == 0; });
+  }
+  std::string why;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaSetDevice(dev);
+    cudaError_t e = cudaDeviceReset();
+    if (e != cudaSuccess) why = std::string("cudaDeviceReset: ") + cudaGetErrorString(e);
+    cudaSetDevice(dev);
+    e = cudaFree(0);
+    if (e != cudaSuccess && why.empty()) why = std::string("context re-creation: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    b2o_ops_forget_device(dev);
+    b2o_gemm_tc_forget_device(dev);
+    b2o_xsum_forget_device(dev);
+    std::vector<Worker *> mine;
+    for (auto &x : g_rt->workers)
+      if (x->device == dev) mine.push_back(x.get());
+    for (Worker *x : mine) {
+      x->stream = nullptr;  // destroyed with the context
+      e = cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess && why.empty()) why = std::string("stream re-creation: ") + cudaGetErrorString(e);
+    }
+    b2o_ops_warm();
+    b2o_gemm_tc_warm();
+    b2o_gemm_warm();
+    b2o_xsum_warm();
+    for (auto &kv : g_rt->apps) {
+      AppShared *a = kv.second.get();
+      if (!a->finalized) continue;
+      for (Worker *x : mine) {
+        // the replica's device memory, pinned buffers, events and module went
+        // with the context: drop the bookkeeping only
+        delete a->per_worker[x->index].release();
+        AppDev *d = nullptr;
+        if (why.empty() && make_replica(a, x, &d, nullptr) != 0) why = "replica rebuild: " + g_err;
+      }
+    }
+    for (Worker *x : mine) {
+      ++x->recoveries;
+      if (why.empty()) {
+        x->broken = false;
+        x->broken_why.clear();
+      } else {
+        x->broken = true;
+        x->broken_why = "device reset after a sticky error failed: " + why;
+      }
+    }
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_rt->qmu);
+    g_rt->paused.erase(dev);
+  }
+  g_rt->qcv.notify_all();
+}
+
 void worker_loop(Worker *w) {
   cudaSetDevice(w->device);
   for (;;) {
@@ -1009,6 +1136,7 @@ void worker_loop(Worker *w) {
       std::unique_lock<std::mutex> lk(g_rt->qmu);
       g_rt->qcv.wait(lk, [&] {
         if (g_rt->stopping) return true;
+        if (g_rt->paused.count(w->device)) return false;  // the device is being reset
         for (Job *q : g_rt->queue)
           if (q->pat.device < 0 || q->pat.device == w->index) return true;
         return false;
@@ -1018,15 +1146,24 @@ void worker_loop(Worker *w) {
         if ((*it)->pat.device < 0 || (*it)->pat.device == w->index) {
           j = *it;
           g_rt->queue.erase(it);
+          ++g_rt->active[w->device];
           break;
         }
       }
     }
     if (!j) continue;
     execute(w, *j);
-    Batch *b = j->batch;
-    std::lock_guard<std::mutex> lk(b->mu);
-    if (--b->remaining == 0) b->cv.notify_all();
+    {
+      std::lock_guard<std::mutex> q(g_rt->qmu);
+      --g_rt->active[w->device];
+    }
+    g_rt->qcv.notify_all();
+    {
+      Batch *b = j->batch;
+      std::lock_guard<std::mutex> lk(b->mu);
+      if (--b->remaining == 0) b->cv.notify_all();
+    }
+    if (w->broken) recover_device(w);
   }
 }
 
@@ -1108,6 +1245,18 @@ int b2o_init(const int32_t *device_ids, int32_t n) {
 
 int b2o_num_workers(void) { return g_rt ? (int)g_rt->workers.size() : 0; }
 
+int b2o_debug_inject_fault(int32_t worker) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_rt || worker < 0 || worker >= (int)g_rt->workers.size()) return fail("bad worker %d", worker);
+  g_rt->workers[worker]->inject_fault = 1;
+  return 0;
+}
+
+int64_t b2o_worker_recoveries(int32_t worker) {
+  if (!g_rt || worker < 0 || worker >= (int)g_rt->workers.size()) return -1;
+  return (int64_t)g_rt->workers[worker]->recoveries;
+}
+
 int b2o_shutdown(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_rt) return 0;
@@ -1122,20 +1271,7 @@ int b2o_shutdown(void) {
     AppShared *a = kv.second.get();
     for (auto &d : a->per_worker) {
       if (!d) continue;
-      cudaSetDevice(d->w->device);
-      for (void *p : d->dev_alloc) if (p) cudaFree(p);
-      for (void *p : d->dev_pristine) if (p) cudaFree(p);
-      for (size_t v = 0; v < d->host.size(); ++v)
-        if (a->info->vars[v].is_array && d->host[v]) cudaFreeHost(d->host[v]);
-      if (d->cells) cudaFreeHost(d->cells);
-      if (d->slab_init) cudaFreeHost(d->slab_init);
-      if (d->slab) cudaFree(d->slab);
-      if (d->scratch) cudaFree(d->scratch);
-    for (void *p : d->red_bufs) if (p) cudaFree(p);
-    if (d->xsum_ws) cudaFree(d->xsum_ws);
-      for (void *p : d->red_bufs) if (p) cudaFree(p);
-      if (d->xsum_ws) cudaFree(d->xsum_ws);
-      if (d->mod) drv.moduleUnload(d->mod);
+      free_app_dev(a, d.get());
     }
   }
   for (auto &w : g_rt->workers) {
@@ -1260,17 +1396,7 @@ int b2o_app_destroy(uint64_t app) {
     if (!d) continue;
     cudaSetDevice(d->w->device);
     cudaStreamSynchronize(d->w->stream);
-    for (void *p : d->dev_alloc) if (p) cudaFree(p);
-    for (void *p : d->dev_pristine) if (p) cudaFree(p);
-    for (size_t v = 0; v < d->host.size(); ++v)
-      if (a->info->vars[v].is_array && d->host[v]) cudaFreeHost(d->host[v]);
-    if (d->cells) cudaFreeHost(d->cells);
-    if (d->slab_init) cudaFreeHost(d->slab_init);
-    if (d->slab) cudaFree(d->slab);
-    if (d->scratch) cudaFree(d->scratch);
-    for (void *p : d->red_bufs) if (p) cudaFree(p);
-    if (d->xsum_ws) cudaFree(d->xsum_ws);
-    if (d->mod) drv.moduleUnload(d->mod);
+    free_app_dev(a, d.get());
   }
   if (a->dl) dlclose(a->dl);
   g_rt->apps.erase(app);

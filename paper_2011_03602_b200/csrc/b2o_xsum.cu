@@ -536,6 +536,7 @@ struct Workspace {
 };
 std::mutex ws_mu;
 std::map<int, Workspace> ws_by_dev;
+std::atomic<bool> g_attr[2][64];  // per (format, device) smem attribute set (cleared on device reset)
 
 struct Layout {
   int64_t nchunks, nsupers;
@@ -573,7 +574,7 @@ int exact_sum_ws(const typename T::V *x, int64_t n, typename T::V s0, typename T
   int *ebase = (int *)(ws + L.ebase);
   Summ<T> *chunks = (Summ<T> *)(ws + L.chunks), *supers = (Summ<T> *)(ws + L.supers);
   constexpr int kSummSmem = XS_SUPER * (XS_CHUNK + XS_CHUNK / 32) * (int)sizeof(V);
-  static std::atomic<bool> attr[64];
+  std::atomic<bool> *attr = g_attr[sizeof(typename T::V) == 8];
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
@@ -642,6 +643,15 @@ extern "C" int b2o_exact_sum_f64(const double *x, int64_t n, double s0, double *
 
 // force-load this file's kernels (lazy module loading would otherwise charge
 // the first timed pattern that uses one); called per device by b2o_init
+// the device was reset (runtime broken-worker recovery): drop its workspace
+// and attribute flags
+extern "C" void b2o_xsum_forget_device(int dev) {
+  std::lock_guard<std::mutex> lk(ws_mu);
+  ws_by_dev.erase(dev);
+  g_attr[0][dev & 63] = false;
+  g_attr[1][dev & 63] = false;
+}
+
 extern "C" void b2o_xsum_warm(void) {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, xs_stats_kernel<F32>);

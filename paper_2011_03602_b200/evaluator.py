@@ -186,6 +186,8 @@ class B200Evaluator:
         except (CompileError, B2OError, ValueError) as exc:
             self._apps[key] = exc
             raise
+        except OSError as exc:  # compiler missing, cache disk full: not cached, may be transient
+            raise B2OError(f"I/O failure while building the program: {exc}") from exc
         self._apps[key] = app
         return app
 

@@ -88,6 +88,8 @@ def lib() -> ctypes.CDLL:
             "b2o_shutdown": ([], ctypes.c_int),
             "b2o_last_error": ([], ctypes.c_char_p),
             "b2o_num_workers": ([], ctypes.c_int),
+            "b2o_debug_inject_fault": ([ctypes.c_int32], ctypes.c_int),
+            "b2o_worker_recoveries": ([ctypes.c_int32], ctypes.c_int64),
             "b2o_abi_version": ([], ctypes.c_int),
             "b2o_app_create": ([ctypes.c_char_p, ctypes.c_char_p, u64p], ctypes.c_int),
             "b2o_app_set_initial": ([ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_uint64], ctypes.c_int),
@@ -157,10 +159,17 @@ class Runtime:
         with cls._ilock:
             if cls._instance is None:
                 cls._instance = Runtime(devices)
-            elif devices is not None and cls._instance.devices not in (None, devices) and \
-                    len(devices) != cls._instance.n_workers:
-                raise B2OError(f"runtime already initialised on {cls._instance.devices}")
+            elif devices is not None and list(devices) != cls._current_devices():
+                # one worker pool per process: a different device set would
+                # silently run on the wrong GPUs
+                raise B2OError(f"runtime already initialised on devices {cls._current_devices()}, "
+                               f"requested {list(devices)}")
             return cls._instance
+
+    @classmethod
+    def _current_devices(cls) -> list[int]:
+        inst = cls._instance
+        return list(inst.devices) if inst.devices else list(range(inst.n_workers))
 
     @classmethod
     def shutdown(cls) -> None:
@@ -168,6 +177,9 @@ class Runtime:
             if cls._instance is not None:
                 lib().b2o_shutdown()
                 cls._instance = None
+
+
+FLAG_INPUTS_RESIDENT = 2  # include/b2o.h B2O_FLAG_INPUTS_RESIDENT
 
 
 class NativeApp:
@@ -225,7 +237,8 @@ class NativeApp:
             arr[i] = Pattern(ctypes.cast(roots, ctypes.POINTER(ctypes.c_uint8)), self.n_loops, len(dirs),
                              ctypes.cast(darr, ctypes.POINTER(Directive)), float(p.get("priority", 0.0)),
                              float(p.get("timeout_s", 0.0) or 0.0), int(p.get("device", -1)),
-                             MODE[p.get("mode", "coherent")], int(p.get("repeats", 1)), 0)
+                             MODE[p.get("mode", "coherent")], int(p.get("repeats", 1)),
+                             FLAG_INPUTS_RESIDENT if p.get("inputs_resident") else 0)
         return arr, keep
 
     def run(self, patterns: list[dict]) -> list[dict]:

@@ -80,6 +80,30 @@ class _BatchRunner:
         return self._Request(model=self.model, pattern=pattern, transfer_plan=plan, emitted_code=code,
                              backend=self.backend, replaced_blocks=self.replaced_blocks, tags=dict(tags))
 
+    def _measure_all(self, requests) -> list:
+        """Measure a batch; an ``OSError`` out of the evaluator (harness I/O,
+        a missing compiler, a full disk) makes the affected requests
+        ``runtime_error`` instead of aborting the search, as the reference's
+        ``GenomeEvaluator.evaluate`` does (src/ga.py:124-128)."""
+        if not requests:
+            return []
+        measure_batch = getattr(self.evaluator, "measure_batch", None)
+        if measure_batch is not None:
+            try:
+                return measure_batch(requests)
+            except OSError:
+                pass  # re-measure one by one so only the failing requests are infeasible
+        return [self._measure_one(r) for r in requests]
+
+    def _measure_one(self, request):
+        from gpuoffload.evaluators import MeasurementResult
+
+        try:
+            return self.evaluator.measure(request)
+        except OSError as exc:
+            return MeasurementResult(None, "runtime_error", getattr(self.evaluator, "evaluator_id", "unknown"),
+                                     f"evaluator I/O failure: {exc}")
+
     def evaluate_population(self, population, tags) -> list:
         """Fitness of every individual, in population order.  First
         occurrences of uncached genomes are measured together; repeats (in
@@ -106,14 +130,7 @@ class _BatchRunner:
                     extra.append(tuple(g))
         batch = to_measure + extra
         requests = [self._request(b, tags) for b in batch]
-        if requests:
-            measure_batch = getattr(self.evaluator, "measure_batch", None)
-            if measure_batch is not None:
-                results = measure_batch(requests)
-            else:
-                results = [self.evaluator.measure(r) for r in requests]
-        else:
-            results = []
+        results = self._measure_all(requests)
         for bits, req, res in zip(batch, requests, results):
             if bits in seen:
                 fresh_res[bits] = (req, res)

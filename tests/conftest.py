@@ -33,3 +33,28 @@ def has_reference() -> bool:
         return True
     except ImportError:
         return False
+
+
+_FINAL: dict = {}
+
+
+def oracle_final(doc: dict, spec: dict) -> dict:
+    """Final state of a program by the reference's own C emission
+    (oracle/_ref, prebuilt by __graft_entry__.build() and travelling with the
+    snapshot), falling back to the C restatement oracle/cgen.py (pinned to
+    the emission bit for bit by tests/test_refc.py) when no object was
+    prebuilt for this document.  Cached per (document, precision, inputs)."""
+    import hashlib
+
+    from oracle.externals import make_binder
+    from oracle.refc import reference_state
+    from paper_2011_03602_b200 import appspec
+    from paper_2011_03602_b200.ir import Program
+
+    # the spec's inputs matter: fuzz programs share documents and differ by seeds
+    key = hashlib.sha256((json.dumps(doc, sort_keys=True) + spec.get("precision", "fp32")
+                          + json.dumps(spec.get("inputs", {}), sort_keys=True)).encode()).hexdigest()
+    if key not in _FINAL:
+        st = appspec.initial_state(Program(doc), spec)
+        _FINAL[key] = reference_state(doc, spec, st, make_binder(doc, spec))[0]
+    return _FINAL[key]

@@ -4,16 +4,15 @@ fp32 reductions; fixtures with the reference's screen verdicts and hoisted
 plans for every genome, tests/golden/fuzz_shapes.json).
 
 CPU: the programs really exercise those shapes.  GPU: every genome of every
-program is valid and leaves exactly the C oracle's final state."""
+program is valid and leaves exactly the final state of the reference's own C emission
+(oracle/_ref; tests/conftest.py oracle_final)."""
 
 import json
 
 import numpy as np
 import pytest
 
-from conftest import GOLDEN
-from oracle.cgen import CProgram
-from paper_2011_03602_b200 import appspec
+from conftest import GOLDEN, oracle_final
 from paper_2011_03602_b200.ir import Program
 
 SHAPES = json.loads((GOLDEN / "fuzz_shapes.json").read_text())
@@ -44,8 +43,7 @@ def test_every_genome_bit_exact(seed):
 
     r = SHAPES[seed]
     prog = Program(r["doc"])
-    st = appspec.initial_state(prog, r["spec"])
-    want = CProgram(r["doc"]).run(st)
+    want = oracle_final(r["doc"], r["spec"])
     ev = B200Evaluator(r["spec"], devices=[0])
     app = ev.app_for(r["doc"])
     outs = [prog.var_by_name[o].id for o in r["spec"]["outputs"]]

@@ -10,9 +10,7 @@ import json
 
 import pytest
 
-from conftest import GOLDEN
-from oracle.cgen import CProgram
-from paper_2011_03602_b200 import appspec
+from conftest import GOLDEN, oracle_final
 from paper_2011_03602_b200.ir import Program
 
 OPTIONS = [
@@ -71,7 +69,7 @@ def test_option_every_genome_bit_exact(opt):
     for name, doc, spec, patterns in PROGRAMS:
         sp = dict(copy.deepcopy(spec), **opt)
         prog = Program(doc)
-        want = CProgram(doc, sp.get("precision", "fp32")).run(appspec.initial_state(prog, sp))
+        want = oracle_final(doc, sp)
         ev = B200Evaluator(sp, devices=[0])
         app = ev.app_for(doc)
         outs = [prog.var_by_name[o].id for o in sp["outputs"]]

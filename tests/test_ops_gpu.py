@@ -44,7 +44,7 @@ def test_tcgen05_gemm_matches_float64(torch_cuda, m, n, k):
     # 3xTF32 with chunked TMEM accumulation: ~1e-6 norm-wise independent of
     # K (a single TMEM accumulator reached 1e-5 at K=1024; plain TF32 ~1e-4)
     assert normwise < 3e-6, normwise
-    assert elem < 5e-5, elem
+    assert elem < 1e-5, elem  # the reference's element-wise rule at fp32 (U[0,1) inputs)
 
 
 def test_tcgen05_gemm_signed_inputs(torch_cuda):

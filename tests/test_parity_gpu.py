@@ -1,6 +1,8 @@
 """GPU parity: every genome of every small app, executed through the C ABI
-(B200Evaluator -> libb2o.so -> compiled sm_100a kernels), must reproduce the C
-oracle's final state (oracle/cgen.py, itself pinned to oracle/interp.py) and
+(B200Evaluator -> libb2o.so -> compiled sm_100a kernels), must reproduce, bit for bit,
+the final state of the reference's own C emission (oracle/_ref; the C
+restatement oracle/cgen.py where none was prebuilt, pinned to it by
+tests/test_refc.py) and
 execute exactly the plan's directive multiplicities
 (``TransferDirective.multiplicity``, src/transfers.py:176-188)."""
 
@@ -9,7 +11,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import SMALL_APPS, golden
+from conftest import SMALL_APPS, golden, oracle_final
 
 pytestmark = pytest.mark.gpu
 
@@ -21,15 +23,9 @@ def oracle_cache():
 
 def _oracle_state(name, g, cache):
     if name not in cache:
-        from oracle.cgen import CProgram
-        from oracle.externals import make_binder
-        from paper_2011_03602_b200 import appspec
         from paper_2011_03602_b200.ir import Program
 
-        prog = Program(g["doc"])
-        state = appspec.initial_state(prog, g["spec"])
-        cache[name] = (prog, CProgram(g["doc"], g["spec"].get("precision", "fp32")).run(
-            state, make_binder(g["doc"], g["spec"])))
+        cache[name] = (Program(g["doc"]), oracle_final(g["doc"], g["spec"]))
     return cache[name]
 
 
@@ -46,12 +42,6 @@ def evaluators():
         return made[key]
 
     return get
-
-
-def _close(a, b, rel):
-    a = np.asarray(a, dtype=np.float64)
-    b = np.asarray(b, dtype=np.float64)
-    return np.all(np.abs(a - b) <= np.maximum(rel * np.abs(b), 1e-12))
 
 
 @pytest.mark.parametrize("name", SMALL_APPS)
@@ -78,7 +68,7 @@ def test_all_genomes_match_oracle(name, evaluators, oracle_cache):
         r = ev.measure_payloads(g["doc"], [g["patterns"][x]])[0]
         for vid in outputs:
             got = app.read(vid, worker=r["worker"])
-            assert _close(got, want[vid], 1e-5), (name, x, prog.vars[vid].name)
+            assert got.tobytes() == np.asarray(want[vid], dtype=got.dtype).tobytes(), (name, x, prog.vars[vid].name)
 
 
 def test_himeno_bit_exact(evaluators, oracle_cache):
@@ -152,3 +142,57 @@ def test_pattern_for_another_program_is_rejected(evaluators):
     ev = evaluators("blocks_nest64", g["spec"])
     r = ev.measure_payloads(variant["doc"], [{"gpu_roots": [0], "directives": []}])[0]
     assert r["validity"] in ("compile_error", "runtime_error"), r
+
+
+RESET_SRC = """int i;
+int j;
+float a[4096];
+float b[4096];
+float c[4096];
+
+func main() {
+  for (i = 0; i < 2048; i++) {
+    b[i] = a[i] * 2.0;
+  }
+  for (j = 0; j < 4096; j++) {
+    c[j] = b[j] + 1.0;
+  }
+  for (i = 2048; i < 4096; i++) {
+    b[i] = a[i] * 3.0;
+  }
+}
+"""
+
+
+def test_reset_restores_device_only_intermediates():
+    """an array a kernel writes but the host never reads
+    (b: not an output, never downloaded) must be back to its pristine value
+    on the device at the start of the next job.  Nest 1 writes b's first
+    half, nest 2 reads all of b, nest 3 writes the second half: the second
+    and later runs of the same pattern on the same worker used to read the
+    previous run's second half."""
+    from gpuoffload.evaluators import EvaluationRequest
+    from gpuoffload.irdoc import model_to_document
+    from gpuoffload.minilang import parse_mini_source
+    from gpuoffload.patterns import build_genome_space, pattern_from_genome
+    from gpuoffload.screen import screen_model
+    from gpuoffload.transfers import plan_transfers
+
+    from paper_2011_03602_b200.evaluator import B200Evaluator, payload_from_request
+    from paper_2011_03602_b200.ir import Program
+
+    model = parse_mini_source(RESET_SRC)
+    doc = model_to_document(model)
+    spec = {"precision": "fp32", "inputs": {"a": {"kind": "uniform", "seed": 5}}, "outputs": {"c": {"rel_tol": 0.0}}}
+    space = build_genome_space(model, screen_model(model))
+    ev = B200Evaluator(spec, devices=[0])
+    want = oracle_final(doc, spec)
+    cid = Program(doc).var_by_name["c"].id
+    app = ev.app_for(doc)
+    for bits in [(1, 1, 1), (1, 1, 1), (1, 0, 1), (1, 1, 1), (0, 1, 0), (1, 1, 1)]:
+        pat = pattern_from_genome(model, space, bits)
+        req = EvaluationRequest(model, pat, plan_transfers(model, pat), "", "c_openacc")
+        r = ev.measure_payloads(doc, [payload_from_request(req)])[0]
+        assert r["validity"] == "valid", (bits, r["diag"])
+        got = app.read(cid, worker=r["worker"])
+        assert got.tobytes() == want[cid].tobytes(), bits

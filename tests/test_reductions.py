@@ -86,11 +86,9 @@ def test_compiler_off_by_default():
 
 
 def _oracle(g):
-    from oracle.cgen import CProgram
+    from conftest import oracle_final
 
-    prog = Program(g["doc"])
-    st = appspec.initial_state(prog, g["spec"])
-    return prog, CProgram(g["doc"], g["spec"].get("precision", "fp32")).run(st)
+    return Program(g["doc"]), oracle_final(g["doc"], g["spec"])
 
 
 def test_exact_reductions_selected():

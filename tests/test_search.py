@@ -55,6 +55,46 @@ def test_batched_ga_equals_reference(seed):
     assert sum(ev.batches) == b.evaluations_performed
 
 
+class FlakyIO(BatchCost):
+    """Raises OSError (harness I/O) for genomes whose first bit is 1."""
+
+    def _boom(self, r):
+        if r.pattern.bits and r.pattern.bits[0] == 1:
+            raise OSError("disk full")
+
+    def measure(self, r):
+        self._boom(r)
+        return self.inner.measure(r)
+
+    def measure_batch(self, rs):
+        for r in rs:
+            self._boom(r)
+        return super().measure_batch(rs)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_oserror_is_runtime_error_like_reference(seed):
+    """an OSError out of measure() makes that genome infeasible and
+    the search continues (src/ga.py:124-128); the batched driver reproduces
+    the reference's result and log."""
+    from gpuoffload.ga import GAParams, run_search
+    from gpuoffload.screen import screen_model
+
+    from _models import random_model
+    from paper_2011_03602_b200.search import run_search_batched
+
+    model = random_model(random.Random(100 + seed), max_depth=3)
+    params = GAParams(population_size=10, generations=5, seed=seed)
+    log_a, log_b = [], []
+    a = run_search(model, screen_model(model), FlakyIO(), params,
+                   on_evaluation=lambda bits, req, res: log_a.append((bits, res.time_seconds, res.validity)))
+    b = run_search_batched(model, screen_model(model), FlakyIO(), params,
+                           on_evaluation=lambda bits, req, res: log_b.append((bits, res.time_seconds, res.validity)))
+    assert a == b
+    assert log_a == log_b
+    assert any(v == "runtime_error" for _, _, v in log_b)
+
+
 class WideCost(BatchCost):
     """A BatchCost that claims to measure `width` patterns at once."""
 
