@@ -20,6 +20,14 @@ void b2o_ops_warm(void);
 void b2o_gemm_tc_warm(void);
 void b2o_gemm_warm(void);
 void b2o_xsum_warm(void);
+// output comparison on the device (b2o_compare.cu): asynchronous on stream,
+// verdict via b2o_compare_result after synchronisation
+size_t b2o_compare_workspace(void);
+int b2o_compare_device(const void *cand, const void *ref, int64_t n, int elem, int normwise, double tol, void *ws,
+                       void *host_acc, void *stream);
+void b2o_compare_result(const void *host_acc, int normwise, double tol, uint64_t *bad, double *worst);
+void b2o_compare_warm(void);
+
 // forget per-device caches (device allocations, function attributes) after
 // the runtime reset that device (broken-worker recovery)
 void b2o_ops_forget_device(int dev);

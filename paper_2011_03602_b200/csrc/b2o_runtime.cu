@@ -100,6 +100,9 @@ struct AppDev {
   std::vector<int64_t> red_buf_elems;
   void *xsum_ws = nullptr;             // exact-sum workspace (b2o_exact_sum_workspace)
   size_t xsum_ws_bytes = 0;
+  std::vector<void *> dev_ref;         // device copies of the reference outputs (device compare)
+  void *cmp_ws = nullptr;              // device compare accumulator (b2o_compare_workspace)
+  void *cmp_host = nullptr;            // pinned copy of its header
   std::vector<uint8_t> hv, dv, hmod, dev_dirty, host_touched;
   // chunked asynchronous D2H still arriving in host[v] (progressive reads)
   struct Pending {
@@ -745,6 +748,10 @@ int make_replica(AppShared *a, Worker *w, AppDev **out, const AppDev *src = null
       return fail("exact-sum warm-up");
   }
   d->pend.assign(nv, AppDev::Pending{});
+  d->dev_ref.assign(nv, nullptr);
+  if (cudaMalloc(&d->cmp_ws, b2o_compare_workspace()) != cudaSuccess) return fail("compare workspace alloc");
+  if (cudaHostAlloc(&d->cmp_host, b2o_compare_workspace(), cudaHostAllocPortable) != cudaSuccess)
+    return fail("compare result buffer");
   d->async_d2h = getenv("B2O_SYNC_D2H") == nullptr;
   ex.pre_launch = cb_pre_launch;
   ex.launch = cb_launch;
@@ -769,6 +776,9 @@ void free_app_dev(AppShared *a, AppDev *d) {
   if (d->scratch) cudaFree(d->scratch);
   for (void *p : d->red_bufs) if (p) cudaFree(p);
   if (d->xsum_ws) cudaFree(d->xsum_ws);
+  for (void *p : d->dev_ref) if (p) cudaFree(p);
+  if (d->cmp_ws) cudaFree(d->cmp_ws);
+  if (d->cmp_host) cudaFreeHost(d->cmp_host);
   if (d->mod) drv.moduleUnload(d->mod);
   for (auto &p : d->pend)
     for (cudaEvent_t e : p.ev) cudaEventDestroy(e);
@@ -777,6 +787,9 @@ void free_app_dev(AppShared *a, AppDev *d) {
   d->dev_pristine.clear();
   d->host.clear();
   d->red_bufs.clear();
+  d->dev_ref.clear();
+  d->cmp_ws = nullptr;
+  d->cmp_host = nullptr;
   d->cells = nullptr;
   d->slab_init = nullptr;
   d->slab = nullptr;
@@ -902,6 +915,14 @@ double normwise_rel(const T *cand, const T *ref, int64_t n) {
   return std::sqrt(num) / std::max(std::sqrt(den), 1e-300);
 }
 
+// coherent runs compare an array output where it is current: on the device
+// when its HBM copy is valid (no download of data the program never read on
+// the host), else on the host.  LITERAL runs always compare the host copy --
+// what the program's host side actually holds (stale reads show there).
+bool device_compared(AppDev *d, int v) {
+  return d->mode == B2O_MODE_COHERENT && VI(d, v).is_array && d->dv[v] && d->cmp_ws && !getenv("B2O_HOST_COMPARE");
+}
+
 void compare_outputs(AppDev *d, b2o_result &r) {
   AppShared *a = d->app;
   const b2o_module_info *info = a->info;
@@ -918,7 +939,26 @@ void compare_outputs(AppDev *d, b2o_result &r) {
     const void *ref = it->second.data();
     uint64_t nbad = 0;
     double w = 0.0;
-    if (oi.mode == B2O_CMP_NORMWISE) {
+    if (device_compared(d, oi.var)) {
+      // the run left the output current in HBM: compare it there against a
+      // device copy of the reference (uploaded once per replica)
+      const int normwise = oi.mode == B2O_CMP_NORMWISE;
+      if (!d->dev_ref[oi.var]) {
+        if (!cuda_ok(d, cudaMalloc(&d->dev_ref[oi.var], it->second.size()), "reference output alloc") ||
+            !cuda_ok(d, cudaMemcpy(d->dev_ref[oi.var], ref, it->second.size(), cudaMemcpyHostToDevice),
+                     "reference output upload"))
+          return;
+      }
+      if (b2o_compare_device(d->dev[oi.var], d->dev_ref[oi.var], n, vi.elem, normwise, oi.rel_tol, d->cmp_ws,
+                             d->cmp_host, d->w->stream) != 0 ||
+          !cuda_ok(d, cudaStreamSynchronize(d->w->stream), "device compare")) {
+        set_error(d, B2O_RUNTIME_ERROR, "device output comparison failed");
+        r.validity = B2O_RUNTIME_ERROR;
+        snprintf(r.diag, sizeof r.diag, "%s", d->err.c_str());
+        return;
+      }
+      b2o_compare_result(d->cmp_host, normwise, oi.rel_tol, &nbad, &w);
+    } else if (oi.mode == B2O_CMP_NORMWISE) {
       double rel = vi.elem == B2O_I32   ? normwise_rel((const int32_t *)cand, (const int32_t *)ref, n)
                    : vi.elem == B2O_F32 ? normwise_rel((const float *)cand, (const float *)ref, n)
                                         : normwise_rel((const double *)cand, (const double *)ref, n);
@@ -1024,7 +1064,7 @@ void execute(Worker *w, Job &j) {
   const b2o_module_info *info = j.app->info;
   for (int o = 0; o < info->n_outputs; ++o) {
     int v = info->outputs[o].var;
-    if (!d->hv[v] && d->mode == B2O_MODE_COHERENT) {
+    if (!d->hv[v] && d->mode == B2O_MODE_COHERENT && !device_compared(d, v)) {
       copy_d2h(d, v);
       d->hv[v] = 1;
       r.epilogue_bytes += var_bytes(d, v);
@@ -1099,6 +1139,7 @@ void recover_device(Worker *w) {
     b2o_gemm_tc_warm();
     b2o_gemm_warm();
     b2o_xsum_warm();
+    b2o_compare_warm();
     for (auto &kv : g_rt->apps) {
       AppShared *a = kv.second.get();
       if (!a->finalized) continue;
@@ -1236,6 +1277,7 @@ int b2o_init(const int32_t *device_ids, int32_t n) {
     b2o_gemm_tc_warm();
     b2o_gemm_warm();
     b2o_xsum_warm();
+    b2o_compare_warm();
     g_rt->workers.push_back(std::move(w));
   }
   for (auto &w : g_rt->workers) w->th = std::thread(worker_loop, w.get());
@@ -1357,6 +1399,19 @@ int b2o_app_finalize(uint64_t app) {
       a->reference[v].assign((const char *)d->host[v], (const char *)d->host[v] + a->initial[v].size());
     }
   }
+  // device copies of the reference outputs for the on-device comparison,
+  // uploaded now so no measurement call pays for them
+  for (auto &dp : a->per_worker) {
+    cudaSetDevice(dp->w->device);
+    for (int o = 0; o < a->info->n_outputs; ++o) {
+      int v = a->info->outputs[o].var;
+      auto it = a->reference.find(v);
+      if (!a->info->vars[v].is_array || it == a->reference.end() || dp->dev_ref[v]) continue;
+      if (cudaMalloc(&dp->dev_ref[v], it->second.size()) != cudaSuccess ||
+          cudaMemcpy(dp->dev_ref[v], it->second.data(), it->second.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail("reference output upload for %s", a->info->vars[v].name);
+    }
+  }
   return 0;
 }
 
@@ -1384,6 +1439,13 @@ int b2o_app_read(uint64_t app, int32_t worker, int32_t var_id, void *out, uint64
   AppDev *d = a->per_worker[worker].get();
   if (var_id < 0 || var_id >= a->info->n_vars) return fail("bad var id");
   if (bytes != a->initial[var_id].size()) return fail("size mismatch");
+  if (!d->hv[var_id]) {
+    // compared on the device and never downloaded: read the HBM copy
+    cudaSetDevice(d->w->device);
+    const void *src = a->info->vars[var_id].is_array ? d->dev[var_id] : (const char *)d->slab + 8 * var_id;
+    if (cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return fail("device read of var %d", var_id);
+    return 0;
+  }
   memcpy(out, d->host[var_id], bytes);
   return 0;
 }

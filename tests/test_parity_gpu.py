@@ -102,7 +102,9 @@ def test_literal_mode_exposes_unfetched_output(evaluators):
     lit = evaluators("noread_literal", g["spec"], mode="literal").measure_payloads(g["doc"], [pat])[0]
     coh = evaluators("noread_coherent", g["spec"]).measure_payloads(g["doc"], [pat])[0]
     assert lit["validity"] == "numeric_mismatch", lit
-    assert coh["validity"] == "valid" and coh["epilogue_bytes"] > 0, coh
+    # coherent: p is current in HBM, so it is compared there (no epilogue
+    # download of data the program never read on the host)
+    assert coh["validity"] == "valid" and coh["epilogue_bytes"] == 0, coh
 
 
 def test_literal_equals_coherent_when_plan_is_complete(evaluators):
@@ -196,3 +198,50 @@ def test_reset_restores_device_only_intermediates():
         assert r["validity"] == "valid", (bits, r["diag"])
         got = app.read(cid, worker=r["worker"])
         assert got.tobytes() == want[cid].tobytes(), bits
+
+
+@pytest.mark.parametrize("name,genome,out,normwise", [("himeno_17x9x33", "100100", "p", False),
+                                                     ("himeno_17x9x33", "000000", "p", False),
+                                                     ("blocks_small", None, "y", True)])
+def test_device_compare_equals_host_compare(name, genome, out, normwise):
+    """The output check on the device (csrc/b2o_compare.cu) gives the host
+    check's verdict, mismatch count and worst relative error (reference rule
+    src/evaluators.py:129-139), for a reference perturbed by small and large
+    relative errors and a NaN."""
+    import os
+
+    from paper_2011_03602_b200 import appspec
+    from paper_2011_03602_b200.evaluator import B200Evaluator
+    from paper_2011_03602_b200.ir import Program
+
+    g = golden(name)
+    if genome is None:
+        v = next(x for x in g["variants"] if x["subset"])
+        doc, pat = v["doc"], v["pattern"]
+    else:
+        doc, pat = g["doc"], g["patterns"][genome]
+    prog = Program(doc)
+    vid = prog.var_by_name[out].id
+    good = oracle_final(doc, g["spec"])[vid] if genome else None
+    if good is None:
+        ev0 = B200Evaluator(g["spec"], devices=[0])
+        ev0.measure_payloads(doc, [pat])
+        good = ev0.app_for(doc).reference(vid)
+    bad = np.array(good, dtype=np.float32, copy=True)
+    idx = np.flatnonzero(np.abs(bad) > 0.1)
+    bad[idx[:5]] *= np.float32(1 + 2e-6)      # within rel_tol 1e-5
+    bad[idx[5:9]] *= np.float32(1.5 if normwise else 1 + 1e-3)  # mismatches
+    if not normwise:
+        bad[idx[9]] = np.nan
+    got = {}
+    for host in (False, True):
+        if host:
+            os.environ["B2O_HOST_COMPARE"] = "1"
+        try:
+            ev = B200Evaluator(g["spec"], devices=[0], reference_outputs={out: bad})
+            r = ev.measure_payloads(doc, [pat])[0]
+        finally:
+            os.environ.pop("B2O_HOST_COMPARE", None)
+        got[host] = (r["validity"], r["mismatches"], r["max_rel_err"])
+    assert got[False] == got[True], got
+    assert got[False][0] == "numeric_mismatch"
