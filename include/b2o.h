@@ -120,7 +120,18 @@ int b2o_abi_version(void);
 int b2o_debug_inject_fault(int32_t worker);
 int64_t b2o_worker_recoveries(int32_t worker);
 
-/* app = one compiled program (host module + cubin from compiler.py) */
+/* app = one compiled program.  b2o_app_load is SURVEY.md §8(b)'s
+ * app_load(model_json, app_spec_json): the IR document (the reference's
+ * irdoc.model_to_document, src/irdoc.py:95-166) and the app spec (inputs,
+ * outputs, tolerances, block shapes; appspec.py) as JSON text; it runs the
+ * package's compiler as a build step (compile_cli.py; B2O_PYTHON picks the
+ * interpreter, default python3), sets every variable's initial value and
+ * finalises (the all-CPU reference run included).  Status < 0 with the
+ * compiler's reason in b2o_last_error for a program it rejects.
+ * b2o_app_create is the lower level: a prebuilt host module + cubin. */
+int b2o_app_load(const char *model_json, const char *app_spec_json, uint64_t *app);
+int b2o_app_num_loops(uint64_t app);                  /* length of b2o_pattern.gpu_root */
+int b2o_app_var_id(uint64_t app, const char *name);   /* variable id by name (< 0: none) */
 int b2o_app_create(const char *host_module, const char *cubin, uint64_t *app);
 int b2o_app_set_initial(uint64_t app, int32_t var_id, const void *data, uint64_t bytes);
 int b2o_app_set_reference(uint64_t app, int32_t var_id, const void *data, uint64_t bytes);

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <cstdlib>
 
 #include <algorithm>
 #include <atomic>
@@ -1337,6 +1338,136 @@ int b2o_app_create(const char *host_module, const char *cubin, uint64_t *app) {
   g_rt->apps[id] = std::move(a);
   *app = id;
   return 0;
+}
+
+// b2o_app_load: the compile service (paper_2011_03602_b200/compile_cli.py)
+// run as a build step, then create + initial state + finalize.
+namespace {
+std::string repo_root() {
+  Dl_info info;
+  if (!dladdr((void *)&b2o_app_load, &info) || !info.dli_fname) return ".";
+  std::string p = info.dli_fname;  // <root>/paper_2011_03602_b200/libb2o.so
+  for (int up = 0; up < 2; ++up) {
+    size_t k = p.find_last_of('/');
+    p = k == std::string::npos ? "." : p.substr(0, k);
+  }
+  return p.empty() ? "/" : p;
+}
+
+bool write_file(const std::string &path, const char *text) {
+  FILE *f = fopen(path.c_str(), "wb");
+  if (!f) return false;
+  size_t n = strlen(text);
+  bool ok = fwrite(text, 1, n, f) == n;
+  return fclose(f) == 0 && ok;
+}
+
+std::string shell_quote(const std::string &s) {
+  std::string o = "'";
+  for (char c : s) o += c == '\'' ? std::string("'\\''") : std::string(1, c);
+  return o + "'";
+}
+}  // namespace
+
+int b2o_app_load(const char *model_json, const char *app_spec_json, uint64_t *app) {
+  if (!model_json || !app_spec_json || !app) return fail("b2o_app_load: null argument");
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_rt) return fail("b2o_init not called");
+  }
+  char dir[] = "/tmp/b2o_load_XXXXXX";
+  if (!mkdtemp(dir)) return fail("b2o_app_load: mkdtemp failed");
+  const std::string d = dir;
+  auto cleanup = [&] { std::system(("rm -rf " + shell_quote(d)).c_str()); };
+  if (!write_file(d + "/doc.json", model_json) || !write_file(d + "/spec.json", app_spec_json)) {
+    cleanup();
+    return fail("b2o_app_load: cannot write the request");
+  }
+  const char *py = getenv("B2O_PYTHON");
+  const std::string root = repo_root();
+  const std::string cmd = "cd " + shell_quote(root) + " && PYTHONPATH=" + shell_quote(root) +
+                          "${PYTHONPATH:+:$PYTHONPATH} " + shell_quote(py && *py ? py : "python3") +
+                          " -m paper_2011_03602_b200.compile_cli " + shell_quote(d + "/doc.json") + " " +
+                          shell_quote(d + "/spec.json") + " " + shell_quote(d) + " 2> " +
+                          shell_quote(d + "/err.txt") + " > /dev/null";
+  const int rc = std::system(cmd.c_str());
+  if (rc != 0) {
+    std::string why;
+    if (FILE *f = fopen((d + "/err.txt").c_str(), "rb")) {
+      char buf[512];
+      size_t n = fread(buf, 1, sizeof buf - 1, f);
+      buf[n] = 0;
+      fclose(f);
+      why = buf;
+    }
+    cleanup();
+    return fail("b2o_app_load: compile service failed (%d): %s", rc, why.c_str());
+  }
+  std::ifstream man(d + "/manifest.txt");
+  std::string kind, host, cubin;
+  struct Init {
+    int id;
+    uint64_t bytes;
+    std::string path;
+  };
+  std::vector<Init> inits;
+  while (man >> kind) {
+    if (kind == "host") man >> host;
+    else if (kind == "cubin") man >> cubin;
+    else if (kind == "loops") { int n; man >> n; }
+    else if (kind == "var") {
+      Init v;
+      std::string name;
+      man >> v.id >> v.bytes >> v.path >> name;
+      inits.push_back(v);
+    } else {
+      std::string rest;
+      std::getline(man, rest);
+    }
+  }
+  if (host.empty() || cubin.empty()) {
+    cleanup();
+    return fail("b2o_app_load: malformed manifest");
+  }
+  uint64_t id = 0;
+  if (b2o_app_create(host.c_str(), cubin.c_str(), &id) != 0) {
+    cleanup();
+    return -1;
+  }
+  for (const Init &v : inits) {
+    std::vector<char> buf(v.bytes);
+    FILE *f = fopen(v.path.c_str(), "rb");
+    bool ok = f && fread(buf.data(), 1, v.bytes, f) == v.bytes;
+    if (f) fclose(f);
+    if (!ok || b2o_app_set_initial(id, v.id, buf.data(), v.bytes) != 0) {
+      cleanup();
+      b2o_app_destroy(id);
+      return ok ? -1 : fail("b2o_app_load: cannot read the initial value of var %d", v.id);
+    }
+  }
+  cleanup();
+  if (b2o_app_finalize(id) != 0) {
+    std::string why = g_err;
+    b2o_app_destroy(id);
+    return fail("%s", why.c_str());
+  }
+  *app = id;
+  return 0;
+}
+
+int b2o_app_num_loops(uint64_t app) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  return a ? a->info->n_loops : fail("unknown app");
+}
+
+int b2o_app_var_id(uint64_t app, const char *name) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  AppShared *a = find_app(app);
+  if (!a || !name) return fail("unknown app");
+  for (int v = 0; v < a->info->n_vars; ++v)
+    if (strcmp(a->info->vars[v].name, name) == 0) return v;
+  return fail("no variable named %s", name);
 }
 
 int b2o_app_set_initial(uint64_t app, int32_t var_id, const void *data, uint64_t bytes) {

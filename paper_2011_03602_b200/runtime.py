@@ -92,6 +92,9 @@ def lib() -> ctypes.CDLL:
             "b2o_worker_recoveries": ([ctypes.c_int32], ctypes.c_int64),
             "b2o_abi_version": ([], ctypes.c_int),
             "b2o_app_create": ([ctypes.c_char_p, ctypes.c_char_p, u64p], ctypes.c_int),
+            "b2o_app_load": ([ctypes.c_char_p, ctypes.c_char_p, u64p], ctypes.c_int),
+            "b2o_app_num_loops": ([ctypes.c_uint64], ctypes.c_int),
+            "b2o_app_var_id": ([ctypes.c_uint64, ctypes.c_char_p], ctypes.c_int),
             "b2o_app_set_initial": ([ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_uint64], ctypes.c_int),
             "b2o_app_set_reference": ([ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_uint64],
                                       ctypes.c_int),

@@ -2,6 +2,8 @@
 declared in include/b2o.h; ctypes struct layouts equal the C layouts."""
 
 import ctypes
+import os
+import sys
 import re
 import subprocess
 from pathlib import Path
@@ -81,3 +83,74 @@ def test_c_consumer_runs():
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
     assert "bit-exact" in r.stdout and "histogram: exact" in r.stdout
+
+
+@pytest.mark.gpu
+def test_c_consumer_loads_and_measures(tmp_path):
+    """The whole boundary from plain C (tests/c/abi_app.c): b2o_app_load
+    from the IR document + app spec JSON (SURVEY.md §8(b) app_load), every
+    Himeno 17x9x33 genome through b2o_submit / b2o_wait, each valid with
+    directive executions == the plan's multiplicities, and each final state
+    bit-identical to the reference's own C emission (oracle/_ref)."""
+    import json
+    import subprocess
+
+    from conftest import golden, oracle_final
+    from paper_2011_03602_b200.ir import Program
+
+    exe = _build_c_consumer().with_name("abi_app")
+    g = golden("himeno_17x9x33")
+    (tmp_path / "doc.json").write_text(json.dumps(g["doc"]))
+    (tmp_path / "spec.json").write_text(json.dumps(g["spec"]))
+    lines = []
+    for genome in sorted(g["patterns"]):
+        p = g["patterns"][genome]
+        lines.append(f"pattern {genome} {len(p['gpu_roots'])} {' '.join(map(str, p['gpu_roots']))} "
+                     f"{len(p['directives'])}")
+        for d in p["directives"]:
+            lines.append(f"{d['var']} {0 if d['dir'] == 'h2d' else 1} {d['anchor_loop']} "
+                         f"{0 if d['side'] == 'before' else 1} {d['multiplicity']} {d['batch']}")
+    (tmp_path / "patterns.txt").write_text("\n".join(lines) + "\n")
+    want = oracle_final(g["doc"], g["spec"])
+    prog = Program(g["doc"])
+    exp = []
+    for name in g["spec"]["outputs"]:
+        arr = want[prog.var_by_name[name].id]
+        f = tmp_path / f"expect_{name}.bin"
+        arr.tofile(f)
+        exp.append(f"{name} {arr.nbytes} {f}")
+    (tmp_path / "expect.txt").write_text("\n".join(exp) + "\n")
+    env = dict(os.environ, B2O_PYTHON=sys.executable)
+    r = subprocess.run([str(exe), str(tmp_path)], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr[-3000:]
+    assert "malformed document refused" in r.stdout
+
+
+def test_compile_service_manifest(tmp_path):
+    """compile_cli (the build step behind b2o_app_load) writes the host
+    module, the cubin and every variable's initial value; a program the
+    compiler cannot take exits 2 with the reason."""
+    import json
+
+    import numpy as np
+
+    from conftest import golden
+    from paper_2011_03602_b200 import appspec, compile_cli
+    from paper_2011_03602_b200.ir import Program
+
+    g = golden("matmul_48")
+    (tmp_path / "doc.json").write_text(json.dumps(g["doc"]))
+    (tmp_path / "spec.json").write_text(json.dumps(g["spec"]))
+    assert compile_cli.main([str(tmp_path / "doc.json"), str(tmp_path / "spec.json"), str(tmp_path / "out")]) == 0
+    man = (tmp_path / "out" / "manifest.txt").read_text().split("\n")
+    assert man[0].startswith("host ") and Path(man[0][5:]).exists()
+    assert man[1].startswith("cubin ") and Path(man[1][6:]).exists()
+    st = appspec.initial_state(Program(g["doc"]), g["spec"])
+    for ln in man[3:]:
+        if not ln:
+            continue
+        _, vid, nbytes, path, name = ln.split()
+        got = np.fromfile(path, dtype=st[int(vid)].dtype)
+        assert got.nbytes == int(nbytes) and np.array_equal(got, st[int(vid)]), name
+    (tmp_path / "bad.json").write_text(json.dumps({"not": "a program"}))
+    assert compile_cli.main([str(tmp_path / "bad.json"), str(tmp_path / "spec.json"), str(tmp_path / "o2")]) == 2
