@@ -42,13 +42,16 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-39"
+COMPILER_VERSION = "b2o-compiler-40"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
 # 258^3: 67.6 -> 53.4 us; tools/kernel_sweep.py, profiles/r01/README.md)
-MARCH_Z = 8
+MARCH_Z = 16  # planes per thread (NAS-MG resid 258^3: 8 -> 51.7 us, 16 -> 50.7 us)
 MARCH_BLOCK = 128
+MARCH_TMA_STAGES = 3   # shared-memory ring depth of the TMA-fed march (planes in flight: stages - 1)
+MARCH_TMA_SPAN = 256   # largest chunk span of one CTA's quads staged (wider CTAs load directly)
+MARCH_TMA_MIN_SPAN = 64  # below this (many streams), the register march kernel instead
 STENCIL_TILE = (32, 8)      # (k, j) tile of the 2.5-D stencil kernels
 BRICK_DEPTH = 4             # outer-loop points per thread in brick kernels
 
@@ -1036,6 +1039,15 @@ class _Gen:
             out.append("    a.chunk = (a.n[0] + chunks - 1) / chunks;")
             out.append(f"    geom[0] = tx; geom[1] = ty; geom[2] = (a.n[0] + a.chunk - 1) / a.chunk; "
                        f"geom[3] = {tk}; geom[4] = {tj}; geom[5] = 1; }}")
+        elif n.shape == "quad" and n.quad.get("march") and self.march_tma(n):
+            # one CTA per (plane block, segment of bt quads of the row space)
+            bt = int(self.spec.get("march_block", MARCH_BLOCK))
+            D = len(n.chain)
+            mid = " * ".join(f"(uint64_t)a.tn[{d}]" for d in range(1, D)) or "1"
+            out.append(f"  {{ uint64_t nseg = ({mid} + {bt - 1}) / {bt}; uint64_t g = (uint64_t)a.tn[0] * nseg;")
+            out.append("    if (g > 0x7FFFFFFFull) { ex->launch(ex, %d, 0, 0, 0); return; }" % lid)
+            out.append(f"    geom[0] = (uint32_t)g; geom[1] = geom[2] = 1; geom[3] = {bt + 32}; "
+                       "geom[4] = geom[5] = 1; }")
         else:
             bt = BLOCK_THREADS
             if n.shape == "quad" and n.quad.get("march"):
@@ -1096,6 +1108,8 @@ class _Gen:
         if n.shape == "ktile":
             return self.ktile_kernel_fn(n)
         if n.shape == "quad" and n.quad.get("march"):
+            if self.march_tma(n):
+                return self.quad_march_tma_kernel_fn(n)
             return self.quad_march_kernel_fn(n)
         if n.shape == "quad":
             return self.quad_kernel_fn(n)
@@ -1418,6 +1432,244 @@ class _Gen:
             out.append(f"    (void)v{v};")
         out.append("  }")
         out.append("}")
+        return out
+
+    def march_streams(self, n: NestPlan) -> list[tuple[int, int, int, int]]:
+        """TMA streams of a plane-march nest: one per (read-only array, plane
+        offset) among the chunks loaded fresh each step, with the chunk-offset
+        range they cover: ``[(v, d, lo, hi)]``."""
+        qp = n.quad
+        mp = qp["march"]
+        keys = mp["keys"]
+        carried = {k for k in keys if (k[0], k[1] + 1, k[2]) in keys and k[0] not in qp["writes"]}
+        rng: dict = {}
+        for v, d, o in keys - carried:
+            if v in qp["writes"] or self.T(v) not in ("float", "int32_t"):
+                continue
+            lo, hi = rng.get((v, d), (o, o))
+            rng[(v, d)] = (min(lo, o), max(hi, o))
+        return [(v, d, lo, hi) for (v, d), (lo, hi) in sorted(rng.items())]
+
+    def march_tma(self, n: NestPlan) -> bool:
+        """The TMA-fed variant (spec ``march_tma``, default OFF: measured
+        slower than the register kernel on NAS-MG resid 258^3 -- 58.8 us at
+        Z=32/4 stages vs 50.7 us, profiles/r02/README.md) applies when the
+        march loads anything fresh per step from read-only arrays."""
+        if not self.spec.get("march_tma", False) or self.spec.get("march_async") or \
+                self.spec.get("march_prefetch"):
+            return False
+        return self.march_tma_span(n) >= MARCH_TMA_MIN_SPAN
+
+    def march_tma_span(self, n: NestPlan) -> int:
+        """Largest per-CTA chunk span the ring can stage within the 48 KB of
+        static shared memory (0: no stream)."""
+        streams = self.march_streams(n)
+        if not streams:
+            return 0
+        P = int(self.spec.get("march_tma_stages", MARCH_TMA_STAGES))
+        budget = (48 * 1024 - 64) // (16 * P)  # chunks per stage
+        fixed = sum(1 + hi - lo for _, _, lo, hi in streams)
+        fit = (budget - fixed) // len(streams) - 1
+        return min(int(self.spec.get("march_tma_span", MARCH_TMA_SPAN)), fit)
+
+    def quad_march_tma_kernel_fn(self, n: NestPlan) -> list[str]:
+        """TMA-fed plane-marching quad kernel.  A CTA owns ``bt`` consecutive
+        quads of the (rows x quads) index space of one block of ``Z`` planes
+        -- consecutive quads are consecutive 16-byte chunks of the flattened
+        arrays, so the chunks every stream of the CTA needs from one plane form
+        ONE contiguous range [bmin + lo, bmax + hi].  An extra producer warp
+        streams those ranges plane by plane with bulk asynchronous copies
+        (``cp.async.bulk``, completion on a "full" mbarrier) into a
+        ``P``-stage shared-memory ring, refilling a stage once every consumer
+        warp has released it ("empty" mbarrier) -- no CTA-wide barrier per
+        step.  Consumer threads read their leading chunks from the ring and
+        carry the rest in registers exactly as the register kernel does
+        (:meth:`quad_march_kernel_fn`).  A CTA whose quads span more than
+        ``MAXSPAN`` chunks (very short rows) loads directly.  Lanes evaluate
+        the same C expression tree (bit-exact)."""
+        prog = self.prog
+        lid = n.root
+        qp = n.quad
+        mp = qp["march"]
+        Z = mp["Z"]
+        C0 = mp["C0"]
+        D = len(n.chain)
+        iv = [prog.loops[c].index_var for c in n.chain]
+        bt = int(self.spec.get("march_block", MARCH_BLOCK))
+        P = int(self.spec.get("march_tma_stages", MARCH_TMA_STAGES))
+        SPAN = self.march_tma_span(n)
+        streams = self.march_streams(n)
+        offs, tot = [], 0
+        for v, d, lo, hi in streams:
+            offs.append(tot)
+            tot += SPAN + 1 + hi - lo
+        NW = bt // 32  # consumer warps
+        out = [f'extern "C" __global__ void __launch_bounds__({bt + 32}) {n.kernel}(const KA_L{lid} a) {{']
+        for v in n.arrays:
+            const = "const " if v not in n.writes else ""
+            out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
+        out.extend(self._locals(n, "  "))
+        out.append(f"  __shared__ __align__(128) int4 ring_[{P}][{tot}];")
+        out.append(f"  __shared__ __align__(8) unsigned long long full_[{P}], empty_[{P}];")
+        out.append("  __shared__ long long bmin_, bmax_;")
+        out.append("  if (threadIdx.x == 0) {")
+        out.append(f"    for (int p_ = 0; p_ < {P}; ++p_) {{ b2o_mbar_init(&full_[p_], 1u); "
+                   f"b2o_mbar_init(&empty_[p_], {NW}u); }}")
+        out.append("    b2o_mbar_fence_init();")
+        out.append("    bmin_ = 0x7fffffffffffffffll; bmax_ = -0x7fffffffffffffffll;")
+        out.append("  }")
+        out.append("  __syncthreads();")
+        mid = " * ".join(f"a.tn[{d}]" for d in range(1, D)) or "1u"
+        out.append(f"  const uint32_t nmid_ = {mid};")
+        out.append(f"  const uint32_t nseg_ = (nmid_ + {bt - 1}u) / {bt}u;")
+        out.append("  const uint32_t zb_ = blockIdx.x / nseg_, seg_ = blockIdx.x - zb_ * nseg_;")
+        out.append(f"  const bool prod_ = threadIdx.x >= {bt}u;  // the producer warp")
+        out.append(f"  const uint32_t tin_ = seg_ * {bt}u + threadIdx.x;")
+        out.append("  bool act_ = !prod_ && tin_ < nmid_ && zb_ < a.tn[0];")
+        out.append("  const uint32_t t = zb_ * nmid_ + tin_;")
+        out.append("  if (act_ && t == a.total - 1u) {")
+        out.extend(self._finals(n, "    "))
+        out.append("  }")
+        out.append("  uint32_t r = act_ ? tin_ : 0u;")
+        for d in range(D - 1, 0, -1):
+            nm = "q_" if d == D - 1 else f"v{iv[d]}_"
+            out.append(f"  uint32_t {nm};")
+            out.append(f"  {{ uint32_t q = b2o_fastdiv(r, a.mul[{d}], a.shr[{d}]); {nm} = r - q * a.tn[{d}]; r = q; }}")
+        out.append(f"  const uint32_t z0_ = zb_ * {Z}u;")
+        out.append(f"  const uint32_t zn_ = zb_ < a.tn[0] ? min({Z}u, a.n[0] - z0_) : 0u;")
+        for d in range(1, D - 1):
+            out.append(f"  const int32_t v{iv[d]} = a.lo[{d}] + (int32_t)v{iv[d]}_;")
+        out.append(f"  int32_t v{iv[0]} = a.lo[0] + (int32_t)z0_;")
+        row = [f"(int64_t){c} * v{v}" for v, c in zip(qp["ovars"], qp["outer"]) if c]
+        out.append(f"  const int64_t F0_ = {' + '.join(row) if row else '0'};")
+        out.append(f"  int64_t b_ = ((F0_ + a.lo[{D - 1}]) & ~(int64_t){QUAD - 1}) + (int64_t){QUAD} * q_;")
+        out.append(f"  const int32_t k0_ = (int32_t)(b_ - F0_);")
+        out.append(f"  const int32_t kr_ = k0_ - a.lo[{D - 1}];")
+        out.append(f"  const int32_t kn_ = (int32_t)a.n[{D - 1}];")
+        out.append(f"  act_ = act_ && !(kr_ + {QUAD - 1} < 0 || kr_ >= kn_);")
+        out.append(f"  const long long bc_ = b_ / {QUAD};")
+        out.append("  if (act_) { atomicMin(&bmin_, bc_); atomicMax(&bmax_, bc_); }")
+        out.append("  __syncthreads();")
+        out.append("  const long long bmin = bmin_, bmax = bmax_;")
+        out.append(f"  const bool tma_ = bmax >= bmin && bmax - bmin <= {SPAN};")
+        out.append("  if (prod_) {")
+        out.append("    // producer: step s (>= 1) of the march into stage (s - 1) % P, after")
+        out.append("    // the consumers released that stage's previous use")
+        out.append("    if (!tma_ || threadIdx.x != " + str(bt) + "u) return;")
+        out.append("    const unsigned ext_ = (unsigned)(bmax - bmin);")
+        nbytes = " + ".join(f"(ext_ + {1 + hi - lo}u)" for _, _, lo, hi in streams)
+        out.append("    for (uint32_t s = 1; s < zn_; ++s) {")
+        out.append(f"      const uint32_t st = (s - 1u) % {P}u, use = (s - 1u) / {P}u;")
+        out.append("      if (use > 0) b2o_mbar_wait(&empty_[st], (use - 1u) & 1u);")
+        out.append(f"      b2o_mbar_expect_tx(&full_[st], 16u * ({nbytes}));")
+        for (v, d, lo, hi), off in zip(streams, offs):
+            out.append(f"      b2o_bulk_g2s(&ring_[st][{off}], reinterpret_cast<const int4 *>(v{v}) + "
+                       f"(bmin + (long long)({d} + (int)s) * {C0 // QUAD} + ({lo})), 16u * (ext_ + {1 + hi - lo}u), "
+                       f"&full_[st]);")
+        out.append("    }")
+        out.append("    return;")
+        out.append("  }")
+        keys = mp["keys"]
+
+        def cname(v, d, o):
+            return f"h{v}_{'m' if d < 0 else ''}{abs(d)}_{'m' if o < 0 else ''}{abs(o)}"
+
+        def ldexpr(v, d, o):
+            vt = "float4" if self.T(v) == "float" else "int4"
+            off = d * C0 // QUAD + o
+            if v in qp["writes"]:
+                return f"(reinterpret_cast<const {vt} *>(v{v} + b_)[{off}])"
+            return f"__ldg(reinterpret_cast<const {vt} *>(v{v} + b_) + ({off}))"
+
+        for v, d, o in sorted(keys):
+            vt = "float4" if self.T(v) == "float" else "int4"
+            zero = "make_float4(0.f, 0.f, 0.f, 0.f)" if vt == "float4" else "make_int4(0, 0, 0, 0)"
+            out.append(f"  {vt} {cname(v, d, o)} = act_ ? {ldexpr(v, d, o)} : {zero};")
+        carried = {k for k in keys if (k[0], k[1] + 1, k[2]) in keys and k[0] not in qp["writes"]}
+        sidx = {}
+        for (v, d, lo, hi), off in zip(streams, offs):
+            for o in range(lo, hi + 1):
+                sidx[(v, d, o)] = off - lo + o
+        out.append("  for (uint32_t s_ = 0; s_ < zn_; ++s_) {")
+        out.append("    if (s_ > 0) {")
+        out.append(f"      b_ += (int64_t){C0}; ++v{iv[0]};")
+        out.append(f"      const uint32_t st_ = (s_ - 1u) % {P}u;")
+        out.append(f"      if (tma_) b2o_mbar_wait(&full_[st_], ((s_ - 1u) / {P}u) & 1u);")
+        out.append("      if (act_) {")
+        for v, d, o in sorted(keys, key=lambda k: (k[1], k[0], k[2])):
+            if (v, d, o) in carried:
+                out.append(f"        {cname(v, d, o)} = {cname(v, d + 1, o)};")
+            elif (v, d, o) in sidx:
+                vt = "float4" if self.T(v) == "float" else "int4"
+                out.append(f"        {cname(v, d, o)} = tma_ ? *reinterpret_cast<const {vt} *>("
+                           f"&ring_[st_][(unsigned)(bc_ - bmin) + {sidx[(v, d, o)]}]) : "
+                           f"{ldexpr(v, d, o)};")
+            else:
+                out.append(f"        {cname(v, d, o)} = {ldexpr(v, d, o)};")
+        out.append("      }")
+        out.append("      if (tma_) {  // this warp is done with the stage")
+        out.append("        __syncwarp();")
+        out.append("        if ((threadIdx.x & 31u) == 0u) b2o_mbar_arrive(&empty_[st_]);")
+        out.append("      }")
+        out.append("    }")
+        out.append("    if (!act_) continue;")
+        out.extend(self._march_compute(n, cname, "    "))
+        out.append("  }")
+        for v in n.locals_:
+            out.append(f"  (void)v{v};")
+        out.append("}")
+        return out
+
+    def _march_compute(self, n: NestPlan, cname, ind: str) -> list[str]:
+        """Lanes and stores of one plane step of a march kernel."""
+        prog = self.prog
+        qp = n.quad
+        mp = qp["march"]
+        kv = prog.loops[n.chain[-1]].index_var
+        ivs = set(qp["ivs"])
+        latest: dict[int, int] = {}
+        out = []
+
+        def lane_expr(e, u):
+            k = e[0]
+            if k == "arr" and e[1] in latest:
+                return f"r{latest[e[1]]}_{u}"
+            if k == "arr":
+                c = affine(e[2], ivs)[1]
+                d, rest = mp["split"](c)
+                el = rest + u
+                return f"{cname(e[1], d, el // QUAD)}.{'xyzw'[el % QUAD]}"
+            if k == "var" and e[1] == kv:
+                return f"(k0_ + {u})"
+            if k in ("num", "var"):
+                return render(e, self.local_name)
+            return f"({lane_expr(e[2], u)} {e[1]} {lane_expr(e[3], u)})"
+
+        body = prog.regions[prog.loops[n.chain[-1]].body].statements
+        for si, st in enumerate(body):
+            v = st.target[1]
+            T = self.T(v)
+            for u in range(QUAD):
+                out.append(f"{ind}const {T} r{si}_{u} = ({T})({lane_expr(st.value, u)});")
+            latest[v] = si
+        for si, st in enumerate(body):
+            v = st.target[1]
+            c = qp["writes"][v]
+            lanes = [f"r{si}_{u}" for u in range(QUAD)]
+            masked = [f"{ind}  if ((uint32_t)(kr_ + {u}) < (uint32_t)kn_) v{v}[b_ + ({c + u})] = r{si}_{u};"
+                      for u in range(QUAD)]
+            if c % QUAD == 0:
+                vt = "float4" if self.T(v) == "float" else "int4"
+                mk = "make_float4" if vt == "float4" else "make_int4"
+                out.append(f"{ind}if (kr_ >= 0 && kr_ + {QUAD} <= kn_) {{")
+                out.append(f"{ind}  reinterpret_cast<{vt} *>(v{v} + b_)[{c // QUAD}] = {mk}({', '.join(lanes)});")
+                out.append(f"{ind}}} else {{")
+                out.extend(masked)
+                out.append(f"{ind}}}")
+            else:
+                out.append(f"{ind}{{")
+                out.extend(masked)
+                out.append(f"{ind}}}")
         return out
 
     def quad_march_kernel_fn(self, n: NestPlan) -> list[str]:
@@ -2230,9 +2482,10 @@ class CompiledApp:
 
 
 def _spec_key(spec: dict) -> dict:
-    return {k: spec.get(k) for k in ("precision", "outputs", "externals", "blocks", "fmad", "stencil",
-                                     "stencil_min_blocks", "flat_ppt", "flat_min_blocks", "flat_kblock",
-                                     "flat_grid_cap", "flat_vec", "quad_groups", "quad_shfl", "quad_shfl_max", "quad_march", "march_block", "march_prefetch", "march_async", "ktile", "progressive_d2h", "exact_reductions", "ktile_tile", "ktile_r", "ktile_ri", "ktile_fast", "ktile_prefetch", "ktile_swz", "reductions")}
+    """Every spec field that can change the generated program: all of them
+    but the input values (initial state, set at load) and the display name.
+    (A whitelist silently dropped new kernel-shape options.)"""
+    return {k: v for k, v in spec.items() if k not in ("inputs", "name")}
 
 
 def build_key(doc: dict, spec: dict) -> str:

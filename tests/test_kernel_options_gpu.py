@@ -34,6 +34,8 @@ OPTIONS = [
     {"ktile_r": 8},
     {"progressive_d2h": False},
     {"flat_min_blocks": 2},
+    {"march_tma": True, "quad_march": 32, "march_tma_stages": 4},
+    {"march_tma": True},
 ]
 
 FUZZ = json.loads((GOLDEN / "fuzz.json").read_text())
