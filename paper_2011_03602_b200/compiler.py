@@ -42,13 +42,15 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-40"
+COMPILER_VERSION = "b2o-compiler-42"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
 # 258^3: 67.6 -> 53.4 us; tools/kernel_sweep.py, profiles/r01/README.md)
-MARCH_Z = 16  # planes per thread (NAS-MG resid 258^3: 8 -> 51.7 us, 16 -> 50.7 us)
+MARCH_Z = 12  # planes per thread (NAS-MG resid 258^3, no prefetch: 8 -> 51.7 us, 16 -> 50.7 us; with the L2 prefetch 12 -> 41.9 us)
 MARCH_BLOCK = 128
+MARCH_FILL = True      # plane-march: carry chunks through unused middle planes (no reloads)
+MARCH_L2PF = 3         # plane-march L2 prefetch distance in planes (0: off; NAS-MG 258: 50.6 -> 42.7 us)
 MARCH_TMA_STAGES = 3   # shared-memory ring depth of the TMA-fed march (planes in flight: stages - 1)
 MARCH_TMA_SPAN = 256   # largest chunk span of one CTA's quads staged (wider CTAs load directly)
 MARCH_TMA_MIN_SPAN = 64  # below this (many streams), the register march kernel instead
@@ -1721,7 +1723,14 @@ class _Gen:
         out.append(f"    const int32_t kn_ = (int32_t)a.n[{D - 1}];")
         out.append(f"    if (kr_ + {QUAD - 1} < 0 || kr_ >= kn_) continue;")
         C0 = mp["C0"]
-        keys = mp["keys"]  # {(v, d, o)} chunks relative to the current plane
+        keys = set(mp["keys"])  # {(v, d, o)} chunks relative to the current plane
+        if self.spec.get("march_fill", MARCH_FILL):
+            # carry a chunk through the planes between its first and last use
+            # (a register move per step) instead of reloading it: NAS-MG's
+            # (j, k-1) and (j, k+4) chunks are read at planes -1 and +1 only
+            for v, o in {(v, o) for v, _, o in keys if v not in qp["writes"]}:
+                ds = [d for w, d, p in keys if w == v and p == o]
+                keys.update((v, d, o) for d in range(min(ds), max(ds) + 1))
 
         def cname(v, d, o):
             return f"h{v}_{'m' if d < 0 else ''}{abs(d)}_{'m' if o < 0 else ''}{abs(o)}"
@@ -1772,6 +1781,30 @@ class _Gen:
                 issue(q, q, "      ")
                 out.append("    }")
                 out.append("    b2o_cp_commit();")
+        # L2 prefetch of the leading plane PF steps ahead (spec ``march_l2pf``):
+        # one prefetch per read-only array at the thread's own chunk of that
+        # plane -- every chunk of a plane is some thread's own, so the whole
+        # plane is requested from DRAM PF steps early without holding
+        # registers; the neighbour-row loads then hit L2.  Guarded to planes
+        # the nest itself reads.
+        PF = int(self.spec.get("march_l2pf", MARCH_L2PF) or 0)
+        pf_lines = []
+        if PF > 0 and not staged:
+            dmax: dict[int, int] = {}
+            for v, d, o in keys:
+                if v not in qp["writes"]:
+                    dmax[v] = max(dmax.get(v, d), d)
+            for v in sorted(dmax):
+                off = (dmax[v] + PF) * C0
+                pf_lines.append(f"{{ const char *pf_ = reinterpret_cast<const char *>(v{v} + b_ + {off}); "
+                                f"asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(pf_)); }}")
+            pf_guard = f"if (v{iv[0]} + {PF} < a.lo[0] + (int32_t)a.n[0])"
+            for q in range(1, PF):  # prologue: the first steps' leading planes
+                out.append(f"    if (v{iv[0]} + {q} < a.lo[0] + (int32_t)a.n[0] && {q}u < zn_) {{")
+                for v in sorted(dmax):
+                    out.append(f"      {{ const char *pf_ = reinterpret_cast<const char *>(v{v} + b_ + "
+                               f"{(dmax[v] + q) * C0}); asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(pf_)); }}")
+                out.append("    }")
         out.append("    for (uint32_t s_ = 0; s_ < zn_; ++s_) {")
         out.append("      if (s_ > 0) {")
         out.append(f"        b_ += (int64_t){C0}; ++v{iv[0]};")
@@ -1797,6 +1830,10 @@ class _Gen:
             else:
                 out.append(f"        {cname(v, d, o)} = {ldexpr(v, d, o)};")
         out.append("      }")
+        if pf_lines:  # b_ is the current plane here
+            out.append(f"      {pf_guard} {{")
+            out.extend("        " + x for x in pf_lines)
+            out.append("      }")
         if pipe:
             out.append("      if (s_ + 1 < zn_) {")
             for v, d, o in lead:

@@ -212,6 +212,9 @@ def main() -> None:
     spec = uniform_spec(m, 11)  # x has 64 floats: no n with 2*n*n == 64, so the FFT variant cannot bind
     (HERE / "blocks_f2.json").write_text(json.dumps(block_record("blocks_f2", m, spec), sort_keys=True) + "\n")
     # cuda_histogram (third DB record): name path (opaque call) + similarity path (loop)
+    # the reference's own pattern DB fixture as data, so the GPU box (no
+    # /root/reference) can drive search_block_combination with it
+    (HERE / "fixtures" / "sample_db.json").write_text((REF / "fixtures" / "sample_db.json").read_text())
     for name, (n, bins) in {"blocks_hist": (4096, 64), "blocks_hist_16m": (1 << 24, 256)}.items():
         m = parse_mini_source(histapp.source(n, bins))
         rec = block_record(name, m, histapp.spec(n, bins))

@@ -8,7 +8,7 @@ import json
 import numpy as np
 import pytest
 
-from conftest import golden, has_reference
+from conftest import GOLDEN, golden, has_reference
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_reference(), reason="reference not importable")]
 
@@ -53,24 +53,40 @@ def test_batched_exhaustive_equals_serial_choices(himeno_xs):
 
 
 def test_block_combination_with_b200():
-    """Name-matched gemm/fft replaced by the hand-written kernels
-    (fixtures/sample_db.json) — every subset valid against the unreplaced
-    program's CPU result."""
-    from gpuoffload.blocks import search_block_combination
+    """The reference's block search itself (src/blocks.py:636-691:
+    search_block_combination -> _measure_subset -> evaluator.measure) driven
+    against B200: name-matched gemm/fft (the reference's fixtures/sample_db.json,
+    committed as tests/golden/fixtures/sample_db.json) replaced by the hand-written
+    kernels; every subset measured valid against the unreplaced program's CPU
+    result, and the chosen subset is the fastest valid one."""
+    from gpuoffload.blocks import (load_pattern_db, match_by_name, match_by_similarity, resolve_candidates,
+                                   search_block_combination)
     from gpuoffload.irdoc import load_ir_document
 
     from paper_2011_03602_b200.evaluator import B200Evaluator
 
     g = golden("blocks_small")
+    base = next(v for v in g["variants"] if not v["subset"])
+    model = load_ir_document(json.dumps(base["doc"]))
+    db = load_pattern_db(GOLDEN / "fixtures" / "sample_db.json")
+    cands, _ = resolve_candidates(model, match_by_name(model, db) + match_by_similarity(model, db))
+    assert [f"{c.block.kind}:{c.block.id}" for c in cands] == [c["block"] for c in g["candidates"]]
     ev = B200Evaluator(g["spec"], devices=[0])
-    results = ev_results = []
+    seen = []
+    out = search_block_combination(model, db, cands, ev,
+                                   on_measure=lambda subset, req, res: seen.append((subset, res)))
+    assert sorted(m.subset for m in out.measurements) == sorted(tuple(v["subset"]) for v in g["variants"])
+    assert len(seen) == len(g["variants"])
+    for m in out.measurements:
+        assert m.result.validity == "valid", (m.subset, m.result)
+        assert m.result.time_seconds > 0
+    best = min(out.measurements, key=lambda m: (m.result.time_seconds, len(m.subset), m.subset))
+    assert out.chosen_subset == best.subset and out.chosen_time == best.result.time_seconds
+    # the replaced subsets ran the block kernels
     for v in g["variants"]:
-        r = ev.measure_payloads(v["doc"], [v["pattern"]])[0]
-        ev_results.append((v["subset"], r))
-    for subset, r in results:
-        assert r["validity"] == "valid", (subset, r["diag"])
-        if subset:
-            assert r["launches"] >= len(subset) and r["block_bytes"] > 0
+        if v["subset"]:
+            r = ev.measure_payloads(v["doc"], [v["pattern"]])[0]
+            assert r["validity"] == "valid" and r["launches"] >= len(v["subset"]) and r["block_bytes"] > 0
 
 
 def test_similarity_matched_gemm_nest():
