@@ -230,7 +230,7 @@ def ref_cpu(g: dict, genome: str | None, runs: int, warm: int = 1, doc: dict | N
     the timer.  Falls back to the C restatement (kind "port") when neither a
     prebuilt object nor the reference package is available."""
     from oracle.externals import make_binder
-    from oracle.refc import RefProgram, RefUnavailable
+    from oracle.refc import BASELINE_FLAGS, RefProgram, RefUnavailable
     from paper_2011_03602_b200 import appspec
     from paper_2011_03602_b200.ir import Program
 
@@ -247,7 +247,7 @@ def ref_cpu(g: dict, genome: str | None, runs: int, warm: int = 1, doc: dict | N
                               genome_loops=g.get("genome_loops"))
         kind = "reference"
         what = ("reference emission gpuoffload.codegen.emit_annotated(c_openacc) of genome "
-                f"{genome}, acc nests as OpenMP, gcc -O2" if openmp
+                f"{genome}, acc nests as OpenMP, gcc {' '.join(BASELINE_FLAGS)}" if openmp
                 else "reference emission gpuoffload.codegen.pretty_print, sequential, gcc -O2")
         for i in range(warm + runs):
             rp.load(state, binder)

@@ -67,6 +67,34 @@ CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fno-buil
           "-mcmodel=medium"]
 
 
+def _baseline_flags() -> list[str]:
+    """The CPU-baseline build (``openmp=True``, the bench's reference arm):
+    as strong as the product's own host build (paper_2011_03602_b200/compiler.py
+    ``_host_flags``) -- -O3 at the widest x86-64 level this machine implements,
+    with the alias-check budget that lets the long stencil statements
+    vectorise -- so the GPU is not compared with a handicapped CPU.  The
+    parity builds keep plain -O2 (results are identical either way: no
+    contraction, no reassociation)."""
+    flags = set()
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("flags"):
+                flags = set(line.split(":", 1)[1].split())
+                break
+    except OSError:
+        pass
+    if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= flags:
+        level = "x86-64-v4"
+    elif {"avx2", "fma", "bmi2", "movbe"} <= flags:
+        level = "x86-64-v3"
+    else:
+        level = "x86-64"
+    return ["-O3", f"-march={level}", "--param", "vect-max-version-for-alias-checks=200"]
+
+
+BASELINE_FLAGS = _baseline_flags()
+
+
 class RefUnavailable(RuntimeError):
     """The reference package is not importable (needed only to emit text)."""
 
@@ -238,6 +266,7 @@ def source(doc: dict, precision: str = "fp32", pattern: dict | None = None, open
 
 def key_of(c: str, precision: str, openmp: bool) -> str:
     return hashlib.sha256((c + precision + str(openmp) + " ".join(CFLAGS)
+                           + (" ".join(BASELINE_FLAGS) if openmp else "")
                            + PRELUDE.read_text()).encode()).hexdigest()[:20]
 
 
@@ -258,7 +287,7 @@ def build(doc: dict, precision: str = "fp32", pattern: dict | None = None, openm
             if precision == "fp64":
                 cmd.append("-Dfloat=double")
             if openmp:
-                cmd.append("-fopenmp")
+                cmd += ["-fopenmp", *BASELINE_FLAGS]
             cmd += [str(OUT / f"ref_{key}.c"), "-o", str(tmp)]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:

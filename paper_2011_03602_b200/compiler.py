@@ -49,6 +49,7 @@ BLOCK_THREADS = 256
 # 258^3: 67.6 -> 53.4 us; tools/kernel_sweep.py, profiles/r01/README.md)
 MARCH_Z = 12  # planes per thread (NAS-MG resid 258^3, no prefetch: 8 -> 51.7 us, 16 -> 50.7 us; with the L2 prefetch 12 -> 41.9 us)
 MARCH_BLOCK = 128
+MARCH_CHAINS = False   # plane-march: carry plane-local subexpressions as scalars
 MARCH_FILL = True      # plane-march: carry chunks through unused middle planes (no reloads)
 MARCH_L2PF = 3         # plane-march L2 prefetch distance in planes (0: off; NAS-MG 258: 50.6 -> 42.7 us)
 MARCH_TMA_STAGES = 3   # shared-memory ring depth of the TMA-fed march (planes in flight: stages - 1)
@@ -1724,6 +1725,96 @@ class _Gen:
         out.append(f"    if (kr_ + {QUAD - 1} < 0 || kr_ >= kn_) continue;")
         C0 = mp["C0"]
         keys = set(mp["keys"])  # {(v, d, o)} chunks relative to the current plane
+        ivs = set(qp["ivs"])
+        body = prog.regions[prog.loops[n.chain[-1]].body].statements
+        # plane-local subexpression chains (spec ``march_chains``): a maximal
+        # subexpression whose array leaves are all read-only and on one plane
+        # (e.g. NAS-MG's u(z-1, j-1, k) + u(z-1, j+1, k)) is evaluated once,
+        # when its plane is the leading plane, and carried to the later steps
+        # as one scalar register instead of its operand chunks -- the same
+        # operations on the same operands in the same order, so the value is
+        # bit-identical; subexpressions equal up to the plane share one chain
+        # (and across lanes and statements).  Frees registers for occupancy.
+        MIX, INV = "mix", "inv"
+        targets = {st.target[1] for st in body}
+        inv_vars = (set(n.scalar_args) - set(n.writes) - targets) | {kv}
+        use_chains = bool(self.spec.get("march_chains", MARCH_CHAINS)) and \
+            not self.spec.get("march_async") and not self.spec.get("march_prefetch")
+
+        def plane_of(e):
+            k = e[0]
+            if k == "num":
+                return INV
+            if k == "var":
+                return INV if e[1] in inv_vars else MIX
+            if k == "arr":
+                if e[1] in targets or e[1] in qp["writes"]:
+                    return MIX
+                return mp["split"](affine(e[2], ivs)[1])[0]
+            a_, b_p = plane_of(e[2]), plane_of(e[3])
+            if MIX in (a_, b_p):
+                return MIX
+            if a_ == INV:
+                return b_p
+            if b_p == INV:
+                return a_
+            return a_ if a_ == b_p else MIX
+
+        def canon(e, u):
+            k = e[0]
+            if k == "arr":
+                el = mp["split"](affine(e[2], ivs)[1])[1] + u
+                return f"a{e[1]}[{el // QUAD}].{'xyzw'[el % QUAD]}"
+            if k == "var" and e[1] == kv:
+                return f"(k0_ + {u})"
+            if k in ("num", "var"):
+                return render(e, self.local_name)
+            return f"({canon(e[2], u)} {e[1]} {canon(e[3], u)})"
+
+        def leaf_chunks(e, u, acc):
+            if e[0] == "arr":
+                el = mp["split"](affine(e[2], ivs)[1])[1] + u
+                acc.add((e[1], el // QUAD))
+            elif e[0] == "bin":
+                leaf_chunks(e[2], u, acc)
+                leaf_chunks(e[3], u, acc)
+            return acc
+
+        chains: dict[str, dict] = {}
+        if use_chains:
+            plain: set = set()
+
+            def collect(e, u):
+                if e[0] == "bin":
+                    pl = plane_of(e)
+                    if pl not in (MIX, INV):
+                        ch = chains.setdefault(canon(e, u), {"e": e, "u": u, "ds": set(),
+                                                             "T": etype(prog, e, self.precision),
+                                                             "leaves": leaf_chunks(e, u, set())})
+                        ch["ds"].add(pl)
+                        return
+                    collect(e[2], u)
+                    collect(e[3], u)
+                elif e[0] == "arr":
+                    d, rest = mp["split"](affine(e[2], ivs)[1])
+                    plain.add((e[1], d, (rest + u) // QUAD))
+
+            for st in body:
+                for u in range(QUAD):
+                    collect(st.value, u)
+            if chains:
+                dmax_v: dict[int, int] = {}
+                for v, d, o in keys:
+                    if v not in qp["writes"]:
+                        dmax_v[v] = max(dmax_v.get(v, d), d)
+                keys = set(plain)
+                for i, (ck, ch) in enumerate(sorted(chains.items())):
+                    ch["name"] = f"p{i}_"
+                    ch["h"] = min(dmax_v[v] for v, _ in ch["leaves"])
+                    ch["dmin"] = min(ch["ds"])
+                    keys |= {(v, ch["h"], o) for v, o in ch["leaves"]}
+            else:
+                use_chains = False
         if self.spec.get("march_fill", MARCH_FILL):
             # carry a chunk through the planes between its first and last use
             # (a register move per step) instead of reloading it: NAS-MG's
@@ -1745,6 +1836,30 @@ class _Gen:
         for v, d, o in sorted(keys):
             vt = "float4" if self.T(v) == "float" else "int4"
             out.append(f"    {vt} {cname(v, d, o)} = {ldexpr(v, d, o)};")
+
+        def dnm(d):
+            return f"{'m' if d < 0 else ''}{abs(d)}"
+
+        def chain_expr(e, u, d, prologue):
+            """the chain's subexpression on plane offset d (chunk registers, or
+            direct loads for prologue planes no chunk register holds)"""
+            k = e[0]
+            if k == "arr":
+                el = mp["split"](affine(e[2], ivs)[1])[1] + u
+                key = (e[1], d, el // QUAD)
+                if key in keys or not prologue:
+                    return f"{cname(*key)}.{'xyzw'[el % QUAD]}"
+                return f"{ldexpr(*key)}.{'xyzw'[el % QUAD]}"
+            if k == "var" and e[1] == kv:
+                return f"(k0_ + {u})"
+            if k in ("num", "var"):
+                return render(e, self.local_name)
+            return f"({chain_expr(e[2], u, d, prologue)} {e[1]} {chain_expr(e[3], u, d, prologue)})"
+
+        for ch in (chains.values() if use_chains else ()):
+            for d in range(ch["dmin"], ch["h"] + 1):
+                out.append(f"    {ch['T']} {ch['name']}{dnm(d)} = ({ch['T']})"
+                           f"{chain_expr(ch['e'], ch['u'], d, True)};")
         carried = {k for k in keys if (k[0], k[1] + 1, k[2]) in keys and k[0] not in qp["writes"]}
         lead = sorted(keys - carried)
         # staged leading plane: each thread copies its own next-plane chunks
@@ -1808,6 +1923,9 @@ class _Gen:
         out.append("    for (uint32_t s_ = 0; s_ < zn_; ++s_) {")
         out.append("      if (s_ > 0) {")
         out.append(f"        b_ += (int64_t){C0}; ++v{iv[0]};")
+        for ch in (chains.values() if use_chains else ()):
+            for d in range(ch["dmin"], ch["h"]):
+                out.append(f"        {ch['name']}{dnm(d)} = {ch['name']}{dnm(d + 1)};")
         if staged:
             # plane s_+P-1 goes out, plane s_ must be in: P-1 younger groups
             # may stay pending
@@ -1829,6 +1947,9 @@ class _Gen:
                 out.append(f"        {cname(v, d, o)} = n{cname(v, d, o)};")
             else:
                 out.append(f"        {cname(v, d, o)} = {ldexpr(v, d, o)};")
+        for ch in (chains.values() if use_chains else ()):
+            h = ch["h"]
+            out.append(f"        {ch['name']}{dnm(h)} = ({ch['T']}){chain_expr(ch['e'], ch['u'], h, False)};")
         out.append("      }")
         if pf_lines:  # b_ is the current plane here
             out.append(f"      {pf_guard} {{")
@@ -1839,11 +1960,14 @@ class _Gen:
             for v, d, o in lead:
                 out.append(f"        n{cname(v, d, o)} = {ldexpr(v, d, o, 1)};")
             out.append("      }")
-        ivs = set(qp["ivs"])
         latest: dict[int, int] = {}
 
         def lane_expr(e, u):
             k = e[0]
+            if use_chains and k == "bin":
+                pl = plane_of(e)
+                if pl not in (MIX, INV):
+                    return f"{chains[canon(e, u)]['name']}{dnm(pl)}"
             if k == "arr" and e[1] in latest:
                 return f"r{latest[e[1]]}_{u}"
             if k == "arr":
@@ -2525,8 +2649,41 @@ def _spec_key(spec: dict) -> dict:
     return {k: v for k, v in spec.items() if k not in ("inputs", "name")}
 
 
+def _host_flags() -> list[str]:
+    """ISA level of the generated host C: the widest x86-64 micro-architecture
+    level this machine implements (part of the module key, so a module built
+    for AVX-512 is never loaded on a host without it), and a higher alias-check
+    budget so the long stencil statements of CPU-resident nests vectorise
+    (gcc gives up on them at its default of 10 runtime checks).  Element-wise
+    vector arithmetic is the scalar arithmetic lane by lane (no contraction,
+    no reassociation: -ffp-contract=off, no -ffast-math), so results stay
+    bit-identical to the reference's emission."""
+    if os.environ.get("B2O_HOST_MARCH"):
+        level = os.environ["B2O_HOST_MARCH"]
+    else:
+        try:
+            flags = set()
+            for line in Path("/proc/cpuinfo").read_text().splitlines():
+                if line.startswith("flags"):
+                    flags = set(line.split(":", 1)[1].split())
+                    break
+        except OSError:
+            flags = set()
+        if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= flags:
+            level = "x86-64-v4"
+        elif {"avx2", "fma", "bmi2", "movbe"} <= flags:
+            level = "x86-64-v3"
+        else:
+            level = "x86-64"
+    return [f"-march={level}", "--param", "vect-max-version-for-alias-checks=200"]
+
+
+HOST_FLAGS = _host_flags()
+
+
 def build_key(doc: dict, spec: dict) -> str:
-    blob = json.dumps({"doc": doc, "spec": _spec_key(spec), "v": COMPILER_VERSION}, sort_keys=True)
+    blob = json.dumps({"doc": doc, "spec": _spec_key(spec), "v": COMPILER_VERSION, "host": HOST_FLAGS},
+                      sort_keys=True)
     return hashlib.sha256(blob.encode()).hexdigest()[:24]
 
 
@@ -2561,8 +2718,8 @@ def compile_program(doc: dict, spec: dict, cache_dir: Path | None = None) -> Com
         fmad = "true" if spec.get("fmad", False) else "false"
         nvcc = os.environ.get("NVCC", "nvcc")
         jobs = [
-            ["g++", "-O3", "-std=c++17", "-shared", "-fPIC", "-ffp-contract=off", "-fno-fast-math", *inc,
-             "app_host.cpp", "-o", "app_host.so"],
+            ["g++", "-O3", "-std=c++17", "-shared", "-fPIC", "-ffp-contract=off", "-fno-fast-math", *HOST_FLAGS,
+             *inc, "app_host.cpp", "-o", "app_host.so"],
             [nvcc, "-cubin", *ARCH_FLAGS, "-O3", "-lineinfo", f"-fmad={fmad}", "-std=c++17", *inc,
              "app_dev.cu", "-o", "app.cubin"],
         ]

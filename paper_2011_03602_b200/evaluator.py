@@ -266,6 +266,21 @@ class B200Evaluator:
     def measure(self, request):
         return self.measure_batch([request])[0]
 
+    def measure_solo(self, request, repeats: int = 3):
+        """One request alone on the worker pool (nothing else in flight),
+        best of ``repeats`` runs, bypassing the program-level dedupe cache:
+        the contention-free fitness a final selection should rest on when the
+        search measured patterns concurrently (``run_search_batched(...,
+        confirm_top=k)``; tools/ga_drift.py measures the drift)."""
+        doc = self._doc(request.model)
+        p = payload_from_request(request)
+        p["repeats"] = max(1, int(repeats))
+        r = dict(self.measure_payloads(doc, [p])[0])
+        r["genome"] = p["genome"]
+        r["solo"] = True
+        self.log.append(r)
+        return self._result(r["validity"], r.get("time_s"), r)
+
     def close(self) -> None:
         for app in self._apps.values():
             if isinstance(app, NativeApp):

@@ -158,11 +158,21 @@ SPECULATE_MAX_BITS = 12  # speculate only in genome spaces of <= 4096 patterns
 
 
 def run_search_batched(model, verdicts, evaluator, params, backend: str = "c_openacc", on_evaluation=None,
-                       speculate: bool | None = None, stats: dict | None = None):
+                       speculate: bool | None = None, stats: dict | None = None, confirm_top: int = 0,
+                       confirm_repeats: int = 3):
     """``run_search`` (src/ga.py:246-285) with per-generation batch
     measurement (and speculative prefetch when ``speculate``; default: on
     when the evaluator is wider than one pattern).  ``stats`` (optional dict)
-    receives ``speculated`` / ``speculated_unused`` counts."""
+    receives ``speculated`` / ``speculated_unused`` counts.
+
+    ``confirm_top=k`` (opt-in; off keeps the reference's final selection):
+    patterns measured concurrently share host cores, host memory bandwidth
+    and PCIe, so their fitness can drift from the solo time (tools/ga_drift.py:
+    <= 9 % with two concurrent patterns, up to 1.6x with eight sharing one
+    B200).  The k fastest feasible genomes are then re-measured one at a time
+    (``evaluator.measure_solo``, best of ``confirm_repeats``; ``measure`` if
+    the evaluator has none) and the fastest confirmed one is returned;
+    ``stats["confirmed"]`` lists (genome, search time, solo time)."""
     ga = _ga()
     from gpuoffload.patterns import PatternError, build_genome_space
 
@@ -188,9 +198,30 @@ def run_search_batched(model, verdicts, evaluator, params, backend: str = "c_ope
     if stats is not None:
         stats.update(speculated=runner.speculated, speculated_unused=len(runner.side))
     best_bits, best_time, no_offload = ga._best_of_cache(runner.cache, space.length)
+    if confirm_top > 0:
+        best_bits, best_time = _confirm(runner, confirm_top, confirm_repeats, best_bits, best_time, stats)
     return ga.SearchResult(best_genome=best_bits, best_time=best_time, no_offload=no_offload,
                            evaluations_performed=runner.evaluations, cache_hits=runner.cache_hits,
                            history=history, genome_length=space.length)
+
+
+def _confirm(runner, k: int, repeats: int, best_bits, best_time, stats):
+    """Re-measure the k fastest feasible genomes alone (see
+    ``run_search_batched``); ties keep the search's order."""
+    ranked = sorted((f.time, bits) for bits, f in runner.cache.items() if f.time is not None)[:k]
+    solo = getattr(runner.evaluator, "measure_solo", None)
+    rows = []
+    for t_search, bits in ranked:
+        req = runner._request(bits, {"confirm": True})
+        res = solo(req, repeats) if solo is not None else runner._measure_one(req)
+        rows.append((bits, t_search, res.time_seconds))
+    if stats is not None:
+        stats["confirmed"] = [("".join(map(str, b)), t, s) for b, t, s in rows]
+    ok = [(s, i, b) for i, (b, _, s) in enumerate(rows) if s is not None]
+    if not ok:
+        return best_bits, best_time
+    s, _, b = min(ok)
+    return b, s
 
 
 def exhaustive_search_batched(model, verdicts, evaluator, cap: int = 14, backend: str = "c_openacc",

@@ -149,6 +149,60 @@ def test_speculation_off_at_width_one():
     assert stats["speculated"] == 0 and sum(ev.batches) == b.evaluations_performed
 
 
+class Drifty(BatchCost):
+    """Batch (concurrent) measurements inflate times by a genome-dependent
+    factor of 1, 1.5 or 2; solo measurements give the true (cost-model)
+    time."""
+
+    def __init__(self):
+        super().__init__()
+        self.solo_calls = []
+
+    def measure_batch(self, rs):
+        from gpuoffload.evaluators import MeasurementResult
+
+        out = []
+        for req, r in zip(rs, super().measure_batch(rs)):
+            k = sum(i * b for i, b in enumerate(req.pattern.bits))
+            out.append(r if r.time_seconds is None else
+                       MeasurementResult(r.time_seconds * (1.0 + 0.5 * (k % 3)), r.validity, r.evaluator_id))
+        return out
+
+    def measure_solo(self, r, repeats):
+        self.solo_calls.append((tuple(r.pattern.bits), repeats))
+        return self.inner.measure(r)
+
+
+def test_confirm_top_reselects_on_solo_times():
+    """confirm_top=k re-measures the k fastest genomes alone and returns the
+    fastest solo time among them; confirm_top=0 keeps the reference's pick."""
+    from gpuoffload.ga import GAParams
+    from gpuoffload.screen import screen_model
+
+    from _models import random_model
+    from paper_2011_03602_b200.search import run_search_batched
+
+    changed = 0
+    for seed in range(6):
+        model = random_model(random.Random(seed), max_depth=3)
+        params = GAParams(population_size=12, generations=6, seed=seed)
+        plain = run_search_batched(model, screen_model(model), Drifty(), params)
+        ev = Drifty()
+        stats = {}
+        conf = run_search_batched(model, screen_model(model), ev, params, stats=stats, confirm_top=4,
+                                  confirm_repeats=2)
+        rows = stats["confirmed"]
+        assert 1 <= len(rows) <= 4 and len(ev.solo_calls) == len(rows)
+        assert all(rep == 2 for _, rep in ev.solo_calls)
+        assert [t for _, t, _ in rows] == sorted(t for _, t, _ in rows)   # the k fastest, in order
+        best = min(s for _, _, s in rows if s is not None)
+        assert conf.best_time == best
+        assert "".join(map(str, conf.best_genome)) in [g for g, _, s in rows if s == best]
+        assert (conf.evaluations_performed, conf.history) == (plain.evaluations_performed, plain.history)
+        changed += conf.best_genome != plain.best_genome
+    assert changed >= 1   # drift changed the pick somewhere (seed 3: 00 -> 01)
+
+
 def test_batched_exhaustive_equals_reference():
     from gpuoffload.evaluators import CostModelEvaluator
     from gpuoffload.ga import exhaustive_search
