@@ -113,10 +113,15 @@ const char *b2o_last_error(void);
 int b2o_num_workers(void);
 int b2o_abi_version(void);
 /* Broken-worker recovery: after a sticky CUDA error the faulting job returns
- * B2O_RUNTIME_ERROR and the runtime resets that device and rebuilds every
- * app replica on it before the next job (b2o_runtime.cu recover_device).
- * b2o_worker_recoveries counts those resets; b2o_debug_inject_fault makes the
- * worker's next job trap on the device (tests only). */
+ * B2O_RUNTIME_ERROR and the runtime tries to reset that device and rebuild
+ * every app replica on it before the next job (b2o_runtime.cu
+ * recover_device).  On the B200 driver measured here the reset cannot bring
+ * the process's context back (profiles/r02/reset_probe.log), so later jobs
+ * on that device return B2O_RUNTIME_ERROR with "device lost" diagnostics;
+ * recovery is then a new process -- paper_2011_03602_b200/isolated.py runs
+ * the runtime in a child it replaces.  b2o_worker_recoveries counts reset
+ * attempts; b2o_debug_inject_fault makes the worker's next job trap on the
+ * device (tests only). */
 int b2o_debug_inject_fault(int32_t worker);
 int64_t b2o_worker_recoveries(int32_t worker);
 

@@ -42,16 +42,16 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-42"
+COMPILER_VERSION = "b2o-compiler-43"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
 # 258^3: 67.6 -> 53.4 us; tools/kernel_sweep.py, profiles/r01/README.md)
 MARCH_Z = 12  # planes per thread (NAS-MG resid 258^3, no prefetch: 8 -> 51.7 us, 16 -> 50.7 us; with the L2 prefetch 12 -> 41.9 us)
 MARCH_BLOCK = 128
-MARCH_CHAINS = False   # plane-march: carry plane-local subexpressions as scalars
+MARCH_CHAINS = True    # plane-march: carry plane-local subexpressions as scalars (NAS-MG resid: 96 -> 72 registers, 41.9 -> 38.7 us)
 MARCH_FILL = True      # plane-march: carry chunks through unused middle planes (no reloads)
-MARCH_L2PF = 3         # plane-march L2 prefetch distance in planes (0: off; NAS-MG 258: 50.6 -> 42.7 us)
+MARCH_L2PF = 2         # plane-march L2 prefetch distance in planes (0: off; NAS-MG 258: 50.6 -> 42.7 us)
 MARCH_TMA_STAGES = 3   # shared-memory ring depth of the TMA-fed march (planes in flight: stages - 1)
 MARCH_TMA_SPAN = 256   # largest chunk span of one CTA's quads staged (wider CTAs load directly)
 MARCH_TMA_MIN_SPAN = 64  # below this (many streams), the register march kernel instead

@@ -266,6 +266,13 @@ class B200Evaluator:
     def measure(self, request):
         return self.measure_batch([request])[0]
 
+    def inject_fault(self, worker: int = 0) -> int:
+        """Tests only: the worker's next job traps on the device (a sticky
+        CUDA error; see isolated.py for what recovers from it)."""
+        from .runtime import lib
+
+        return lib().b2o_debug_inject_fault(int(worker))
+
     def measure_solo(self, request, repeats: int = 3):
         """One request alone on the worker pool (nothing else in flight),
         best of ``repeats`` runs, bypassing the program-level dedupe cache:

@@ -51,6 +51,56 @@ def _ensure_reference_importable() -> None:
             sys.path.append(str(ref))
 
 
+def _reference_file(doc: dict, spec: dict) -> Path:
+    """Where the all-CPU reference outputs of this program (and these inputs)
+    are kept between runner invocations: the harness starts one runner
+    process per pattern, and without the cache every one of them would re-run
+    the whole program on the CPU at load (``b2o_app_finalize``) -- the
+    reference outputs depend on the program and its inputs, never on the
+    genome."""
+    import hashlib
+
+    from .compiler import CACHE
+    from .ir import document_digest
+
+    blob = json.dumps([document_digest(doc), spec.get("inputs"), spec.get("precision"), spec.get("externals"),
+                       sorted(spec.get("outputs", {}))], sort_keys=True, default=str)
+    return Path(CACHE) / "refs" / (hashlib.sha256(blob.encode()).hexdigest()[:24] + ".npz")
+
+
+def _load_reference(path: Path) -> dict | None:
+    import numpy as np
+
+    try:
+        with np.load(path) as z:
+            return {k: z[k] for k in z.files}
+    except (OSError, ValueError):
+        return None
+
+
+def _store_reference(path: Path, ev, doc: dict, spec: dict) -> None:
+    """Written atomically (temp file + rename): concurrent runners may race."""
+    import os
+    import tempfile
+
+    import numpy as np
+
+    from . import appspec
+    from .ir import Program
+
+    try:
+        app = ev.app_for(doc)
+        prog = Program(doc)
+        outs = {prog.vars[vid].name: app.reference(vid) for vid, _, _ in appspec.outputs_of(prog, spec)}
+        path.parent.mkdir(parents=True, exist_ok=True)
+        fd, tmp = tempfile.mkstemp(dir=path.parent, suffix=".npz")
+        with os.fdopen(fd, "wb") as f:
+            np.savez(f, **outs)
+        os.replace(tmp, path)
+    except Exception as exc:  # the cache is an optimisation: never fail the measurement over it
+        print(f"runner: reference cache not written: {exc}", file=sys.stderr)
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--spec", required=True, help="app spec JSON (inputs, outputs, externals, blocks)")
@@ -79,10 +129,14 @@ def main(argv=None) -> int:
         print("runner: placements in pattern.json do not match the rebuilt model", file=sys.stderr)
         return 3
     plan = plan_transfers(model, pattern)
-    ev = B200Evaluator(spec, devices=[args.device], mode=args.mode)
-    req = EvaluationRequest(model, pattern, plan, "", "c_openacc")
     doc = document_of(model)
+    ref_file = _reference_file(doc, spec)
+    cached = _load_reference(ref_file)
+    ev = B200Evaluator(spec, devices=[args.device], mode=args.mode, reference_outputs=cached)
+    req = EvaluationRequest(model, pattern, plan, "", "c_openacc")
     res = ev.measure_payloads(doc, [payload_from_request(req)])[0]
+    if cached is None:
+        _store_reference(ref_file, ev, doc, spec)
     if res["validity"] != "valid":
         print(f"runner: {res['validity']}: {res.get('diag', '')}", file=sys.stderr)
         return 2

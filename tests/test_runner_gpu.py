@@ -49,3 +49,10 @@ def test_cli_pipeline_through_runner(tmp_path):
     # all-CPU program (block-stage baseline, genome None) may well win
     valid = [m["time"] for m in report.measurements if m["validity"] == "valid"]
     assert report.chosen["time"] == min(valid)
+    # the all-CPU reference outputs were computed once and cached for the
+    # later runner processes (one per pattern), keyed by program and inputs
+    from paper_2011_03602_b200.runner import _load_reference, _reference_file
+
+    cached = _load_reference(_reference_file(doc, spec))
+    assert cached is not None and set(cached) == {"chk"}
+    assert cached["chk"].tobytes() == out[prog.var_by_name["chk"].id].tobytes()
