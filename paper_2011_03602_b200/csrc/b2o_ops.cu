@@ -480,9 +480,9 @@ __global__ void __launch_bounds__(256) fft4k_rows_kernel(const float2 *__restric
 // round-trips through HBM.
 constexpr int kClusterFft = 16;
 
-template <int NPC>
-__global__ void __launch_bounds__(256 * NPC) fft4k_cols_cluster_kernel(float2 *__restrict__ y,
-                                                                        const float2 *__restrict__ tw) {
+template <int NPC, int V>
+__global__ void __launch_bounds__(256 * NPC, V == 2 ? 6 / NPC : V == 3 ? 5 / NPC : 0)
+    fft4k_cols_cluster_kernel(float2 *__restrict__ y, const float2 *__restrict__ tw) {
   extern __shared__ float2 s[];  // NPC x 4096
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the rows pass has completed and is visible
   cg::cluster_group cl = cg::this_cluster();
@@ -537,20 +537,28 @@ __global__ void __launch_bounds__(256 * NPC) fft4k_cols_cluster_kernel(float2 *_
       v[m] = peer[k1 * 16 + cc];
     }
     dft16(v);
-    // done reading peers (release: orders the remote loads before the
-    // arrive); the wait at the end keeps this CTA's shared memory alive until
-    // every peer has read it, overlapping the HBM stores
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    // done reading peers; the wait at the end keeps this CTA's shared
+    // memory alive until every peer has read it, overlapping the HBM stores.
+    // V >= 1: a relaxed arrive -- the peer values were consumed by the DFT
+    // above, so the remote loads have completed and need no release fence
+    if (V >= 1)
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    else
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 #pragma unroll
     for (int k = 0; k < 16; ++k) y[(size_t)(k1 + 256 * k) * 4096 + col0 + cc] = v[k];
   }
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
-template <int NPC>
+template <int NPC, int V = 1>
 cudaError_t launch_cols_cluster(float2 *y, const float2 *tw, cudaStream_t s) {
+  static const int v_env = getenv("B2O_FFT_V") ? atoi(getenv("B2O_FFT_V")) : -1;
+  if (V == 1 && v_env == 0) return launch_cols_cluster<NPC, 0>(y, tw, s);
+  if (V == 1 && v_env == 2) return launch_cols_cluster<NPC, 2>(y, tw, s);
+  if (V == 1 && v_env == 3) return launch_cols_cluster<NPC, 3>(y, tw, s);
   constexpr int CL = 16 / NPC;
-  auto kern = fft4k_cols_cluster_kernel<NPC>;
+  auto kern = fft4k_cols_cluster_kernel<NPC, V>;
   const size_t smem = sizeof(float2) * 4096 * NPC;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -690,7 +698,7 @@ extern "C" void b2o_ops_warm(void) {
   cudaFuncGetAttributes(&a, fft16_rows_kernel);
   cudaFuncGetAttributes(&a, fft16_cols_kernel);
   cudaFuncGetAttributes(&a, fft4k_rows_kernel);
-  cudaFuncGetAttributes(&a, (const void *)fft4k_cols_cluster_kernel<1>);
-  cudaFuncGetAttributes(&a, (const void *)fft4k_cols_cluster_kernel<2>);
+  cudaFuncGetAttributes(&a, (const void *)fft4k_cols_cluster_kernel<1, 1>);
+  cudaFuncGetAttributes(&a, (const void *)fft4k_cols_cluster_kernel<2, 1>);
   cudaGetLastError();
 }

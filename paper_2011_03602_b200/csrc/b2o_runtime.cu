@@ -105,6 +105,12 @@ struct AppDev {
   void *cmp_ws = nullptr;              // device compare accumulator (b2o_compare_workspace)
   void *cmp_host = nullptr;            // pinned copy of its header
   std::vector<uint8_t> hv, dv, hmod, dev_dirty, host_touched;
+  // lazy restore: host[v] still holds the previous job's values although the
+  // state is pristine; the pristine bytes are in the app's pinned copy until
+  // a host reader needs host[v] (host_fresh), an upload reads them from the
+  // pinned copy, and a full download overwrites host[v] anyway
+  std::vector<uint8_t> stale;
+  bool lazy_reset = true;
   // chunked asynchronous D2H still arriving in host[v] (progressive reads)
   struct Pending {
     int n = 0, done = 0;
@@ -137,6 +143,7 @@ struct AppShared {
   b2o_mod_run_fn run = nullptr;
   std::vector<char> image;
   std::vector<std::vector<char>> initial;    // per var
+  std::vector<void *> pinned_initial;        // pinned copy of initial[v] (written arrays; lazy restore)
   std::map<int, std::vector<char>> reference;  // per output var
   bool finalized = false;
   double ref_time = -1.0;
@@ -274,8 +281,22 @@ size_t var_bytes(AppDev *d, int v) {
   return vi.is_array ? (size_t)vi.length * elem_bytes(vi.elem) : elem_bytes(vi.elem);
 }
 
+void par_memcpy(void *dst, const void *src, size_t bytes);
+
+// host[v] made pristine before a host reader or writer uses it (lazy reset)
+void host_fresh(AppDev *d, int v) {
+  if (!d->stale[v]) return;
+  const void *src = d->app->pinned_initial[v] ? d->app->pinned_initial[v] : d->app->initial[v].data();
+  par_memcpy(d->host[v], src, d->app->initial[v].size());
+  d->stale[v] = 0;
+}
+
 void copy_h2d(AppDev *d, int v) {
-  cuda_ok(d, cudaMemcpyAsync(d->dev[v], d->host[v], var_bytes(d, v), cudaMemcpyHostToDevice, d->w->stream),
+  // a stale host copy is pristine by definition: upload from the pinned
+  // pristine bytes instead of restoring host[v] first
+  const void *src = d->stale[v] && d->app->pinned_initial[v] ? d->app->pinned_initial[v] : d->host[v];
+  if (d->stale[v] && !d->app->pinned_initial[v]) host_fresh(d, v);
+  cuda_ok(d, cudaMemcpyAsync(d->dev[v], src, var_bytes(d, v), cudaMemcpyHostToDevice, d->w->stream),
           "H2D copy");
   d->dev_dirty[v] = 1;
   d->acc.h2d_bytes += var_bytes(d, v);
@@ -327,6 +348,7 @@ void copy_d2h(AppDev *d, int v, bool async_ok = false) {
     p.chunk = chunk;
     d->acc.d2h_bytes += bytes;
     d->host_touched[v] = 1;
+    d->stale[v] = 0;  // the whole array is overwritten; readers wait for their chunks
     return;
   }
   if (!VI(d, v).is_array && async_ok && d->async_d2h) {
@@ -360,12 +382,16 @@ void copy_d2h(AppDev *d, int v, bool async_ok = false) {
   cuda_ok(d, cudaStreamSynchronize(d->w->stream), "D2H sync");
   d->acc.d2h_bytes += var_bytes(d, v);
   d->host_touched[v] = 1;
+  d->stale[v] = 0;
 }
 
 // make the host copy current (coherent mode); async_ok: the caller waits
 // for the bytes it reads (progressive CPU loops)
 void ensure_host(AppDev *d, int v, bool async_ok = false) {
-  if (d->hv[v]) return;
+  if (d->hv[v]) {
+    host_fresh(d, v);
+    return;
+  }
   if (d->mode == B2O_MODE_LITERAL) {
     d->acc.stale_reads++;
     return;
@@ -421,6 +447,7 @@ void host_access_impl(AppDev *d, int32_t set, const b2o_varset *prog) {
   for (int i = 0; i < wr.n; ++i) wait_host(d, wr.vars[i], SIZE_MAX);
   for (int i = 0; i < wr.n; ++i) {
     int v = wr.vars[i];
+    host_fresh(d, v);
     d->hv[v] = 1;
     d->dv[v] = 0;
     d->hmod[v] = 1;
@@ -718,6 +745,16 @@ int make_replica(AppShared *a, Worker *w, AppDev **out, const AppDev *src = null
   d->hmod.assign(nv, 0);
   d->dev_dirty.assign(nv, 0);
   d->host_touched.assign(nv, 0);
+  d->stale.assign(nv, 0);
+  d->lazy_reset = getenv("B2O_EAGER_RESET") == nullptr;
+  if (a->pinned_initial.size() != (size_t)nv) a->pinned_initial.assign(nv, nullptr);
+  for (int v = 0; v < nv && d->lazy_reset; ++v) {
+    const b2o_var_info &vi = info->vars[v];
+    if (!vi.is_array || !vi.written || a->pinned_initial[v]) continue;
+    if (cudaHostAlloc(&a->pinned_initial[v], a->initial[v].size(), cudaHostAllocPortable) != cudaSuccess)
+      return fail("pinned alloc of the pristine copy of %s", vi.name);
+    memcpy(a->pinned_initial[v], a->initial[v].data(), a->initial[v].size());
+  }
   d->is_root.assign(std::max(nl, 1), 0);
   d->dev_inside.assign(std::max(nl, 1), 0);
   d->hook_mask.assign(std::max(nl, 1), 0);
@@ -822,7 +859,12 @@ void reset_state(AppDev *d) {
     if (!vi.is_array) {
       memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
     } else if (vi.written) {
-      if (d->host_touched[v]) par_memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
+      if (d->host_touched[v]) {
+        if (d->lazy_reset)
+          d->stale[v] = 1;  // restored on first host use (host_fresh), uploads read the pinned copy
+        else
+          par_memcpy(d->host[v], d->app->initial[v].data(), d->app->initial[v].size());
+      }
       // a device copy a kernel or an upload changed is restored whether or
       // not the host ever saw it: prepare_dev_write treats an array the host
       // did not modify since reset as present-by-allocation (pristine), so a
@@ -936,6 +978,7 @@ void compare_outputs(AppDev *d, b2o_result &r) {
     if (it == a->reference.end()) continue;
     const b2o_var_info &vi = info->vars[oi.var];
     int64_t n = vi.is_array ? vi.length : 1;
+    if (!device_compared(d, oi.var)) host_fresh(d, oi.var);
     const void *cand = d->host[oi.var];
     const void *ref = it->second.data();
     uint64_t nbad = 0;
@@ -1316,6 +1359,9 @@ int b2o_shutdown(void) {
       if (!d) continue;
       free_app_dev(a, d.get());
     }
+    for (void *p : a->pinned_initial)
+      if (p) cudaFreeHost(p);
+    a->pinned_initial.clear();
   }
   for (auto &w : g_rt->workers) {
     cudaSetDevice(w->device);
@@ -1577,6 +1623,11 @@ int b2o_app_read(uint64_t app, int32_t worker, int32_t var_id, void *out, uint64
     if (cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return fail("device read of var %d", var_id);
     return 0;
   }
+  if (d->stale[var_id]) {  // untouched since the lazy reset: the pristine bytes
+    const void *src = a->pinned_initial[var_id] ? a->pinned_initial[var_id] : a->initial[var_id].data();
+    memcpy(out, src, bytes);
+    return 0;
+  }
   memcpy(out, d->host[var_id], bytes);
   return 0;
 }
@@ -1591,6 +1642,9 @@ int b2o_app_destroy(uint64_t app) {
     cudaStreamSynchronize(d->w->stream);
     free_app_dev(a, d.get());
   }
+  for (void *p : a->pinned_initial)
+    if (p) cudaFreeHost(p);
+  a->pinned_initial.clear();
   if (a->dl) dlclose(a->dl);
   g_rt->apps.erase(app);
   return 0;
