@@ -12,6 +12,7 @@
 //   n = 256: Stockham radix-16 in shared memory; other powers of two: radix-2.
 // Twiddles are computed in double on the host and kept in a device table.
 #include <cooperative_groups.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -579,6 +580,215 @@ cudaError_t launch_cols_cluster(float2 *y, const float2 *tw, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, y, tw);
 }
 
+// ---- persistent, TMA-fed column pass (opt-in, B2O_FFT_COLS=persist) ---------
+// The cluster kernel above is one load -> compute -> exchange -> store phase
+// per CTA, 4096 short-lived CTAs in 16-CTA clusters: every CTA waits for its
+// own loads and then for the cluster barrier, with little else resident to
+// overlap them (ncu: DRAM 29 % busy, barrier + membar + long-scoreboard
+// stalls).  Here 18 clusters stay resident (2 CTAs per SM, 96 KB smem each)
+// and walk the 256 column groups: CTA rank c's 256 x 16 slice of the next
+// group (rows c + 16 m, one 128-byte segment per row) is fetched by ONE
+// 3-D TMA copy into its input buffer as soon as the current group's first
+// radix-16 pass has read it, so the HBM reads of group g+1 run under the
+// DFTs, the cluster exchange and the stores of group g.  The exchange buffer
+// is double-buffered across groups, so one cluster barrier per group suffices
+// (a CTA passing the barrier of group g+1 knows every peer finished reading
+// its exchange buffer of group g).
+namespace colp {
+
+constexpr int IN_BYTES = 256 * 16 * 8;   // 32 KB: rows c + 16 m, 16 columns
+constexpr int SZ_ELEMS = 4096;           // 32 KB exchange buffer (x2)
+constexpr int SMEM = IN_BYTES + 2 * SZ_ELEMS * 8 + 64;
+
+__device__ __forceinline__ uint32_t su32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint32_t b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint32_t b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, uint32_t b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(b)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(256, 2) fft4k_cols_persist_kernel(float2 *__restrict__ y,
+                                                                     const float2 *__restrict__ tw,
+                                                                     const __grid_constant__ CUtensorMap map,
+                                                                     int nclusters) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  float2 *in = (float2 *)sm;                             // [m][cc]
+  float2 *szb = (float2 *)(sm + IN_BYTES);               // [2][4096]
+  uint64_t *bar = (uint64_t *)(sm + IN_BYTES + 2 * SZ_ELEMS * 8);
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();                    // residue class n2 = c
+  const int cid = (int)(blockIdx.x / 16);
+  const int t = threadIdx.x, cc = t & 15, b = t >> 4;
+  const uint32_t inb = su32(in), barb = su32(bar);
+  if (t == 0) {
+    bar_init(barb, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map) : "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the rows pass has completed and is visible
+  if (t == 0 && cid < 256) {
+    bar_expect(barb, IN_BYTES);
+    tma3(inb, &map, 32 * cid, c, 0, barb);
+  }
+  float2 v[16];
+  int g = 0;
+  for (int p = cid; p < 256; p += nclusters, ++g) {
+    float2 *sz = szb + (g & 1) * SZ_ELEMS;
+    const int col0 = p * 16;
+    bar_wait(barb, g & 1);
+    // pass 1 (DFT over a) from the TMA-landed slice: x[n2 + 16 (b + 16 a)]
+#pragma unroll
+    for (int a = 0; a < 16; ++a) v[a] = in[(b + 16 * a) * 16 + cc];
+    __syncthreads();  // the slice is consumed: fetch the next group's
+    if (t == 0 && p + nclusters < 256) {
+      bar_expect(barb, IN_BYTES);
+      tma3(inb, &map, 32 * (p + nclusters), c, 0, barb);
+    }
+    dft16(v);
+    {
+      const float2 w1 = tw[16 * b];
+      float2 w = w1;
+#pragma unroll
+      for (int k = 1; k < 16; ++k) {
+        v[k] = cmul(v[k], w);
+        w = cmul(w, w1);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) sz[(b * 16 + k) * 16 + cc] = v[k];
+    }
+    __syncthreads();
+    {
+      const int k1a = t >> 4;
+#pragma unroll
+      for (int bb = 0; bb < 16; ++bb) v[bb] = sz[(bb * 16 + k1a) * 16 + cc];
+      __syncthreads();
+      dft16(v);
+      const float2 step = tw[16 * c];
+      float2 w = tw[c * k1a];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        v[k] = cmul(v[k], w);
+        w = cmul(w, step);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) sz[(k1a + 16 * k) * 16 + cc] = v[k];
+    }
+    // publish this group's Y[k1][cc]; passing it also means every peer has
+    // finished reading the other exchange buffer (group g-1)
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    {
+      const int k1 = c * 16 + (t >> 4);
+#pragma unroll
+      for (int m = 0; m < 16; ++m) v[m] = cl.map_shared_rank(sz, m)[k1 * 16 + cc];
+      dft16(v);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) y[(size_t)(k1 + 256 * k) * 4096 + col0 + cc] = v[k];
+    }
+  }
+  // keep the exchange buffers alive until every peer has read them
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) == cudaSuccess)
+      fn = (EncodeFn)q;
+  });
+  return fn;
+}
+
+// the 4096 x 4096 complex64 matrix as a 3-D fp32 tensor: (32 floats = 16
+// complex columns, residue class n2 of the row, row block m), box {32, 1, 256}
+cudaError_t launch(float2 *y, const float2 *tw, cudaStream_t s, int nclusters) {
+  EncodeFn enc = encode();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap map;
+  cuuint64_t dims[3] = {8192, 16, 256};
+  cuuint64_t strides[2] = {8192 * 4, 16 * 8192 * 4};
+  cuuint32_t box[3] = {32, 1, 256};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)y, dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  cudaFuncSetAttribute(fft4k_cols_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaFuncSetAttribute(fft4k_cols_persist_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(16 * nclusters));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = getenv("B2O_PDL") && atoi(getenv("B2O_PDL")) == 0 ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, fft4k_cols_persist_kernel, y, tw, map, nclusters);
+}
+
+// clusters of 16 that fit at once (the occupancy calculator for this exact
+// configuration), capped at the 256 column groups
+int max_clusters(float2 *y, const float2 *tw) {
+  cudaFuncSetAttribute(fft4k_cols_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaFuncSetAttribute(fft4k_cols_persist_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16 * 64);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (const void *)fft4k_cols_persist_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return std::min(n, 256);
+}
+
+}  // namespace colp
+
 std::mutex tw_mu;
 std::map<std::pair<int, int64_t>, float2 *> tw_cache;  // (device, n) -> table
 // per-device "dynamic shared memory attribute set" flags (cleared when the
@@ -624,6 +834,24 @@ extern "C" int b2o_fft2d_c64(const float *x, float *y, int64_t n, void *stream) 
     }
     if (n == 4096 && !getenv("B2O_FFT_LEGACY")) {
       fft4k_rows_kernel<<<4096, 256, 0, s>>>((const float2 *)x, (float2 *)y, tw);
+      // B2O_FFT_COLS=persist: the persistent TMA-fed column pass (measured
+      // slower: 0.157 vs 0.126 ms -- 14 resident clusters leave 21 % of the
+      // warps active, too few to hide the per-group barrier and DSMEM
+      // latency that 5 short-lived CTAs per SM overlap); default: the
+      // per-group cluster kernel below
+      static std::atomic<int> ncl[64];
+      static const bool old_cols = !(getenv("B2O_FFT_COLS") && std::string(getenv("B2O_FFT_COLS")) == "persist");
+      if (!old_cols && ncl[dev & 63] == 0) {
+        int m = colp::max_clusters((float2 *)y, tw);
+        if (getenv("B2O_FFT_CLUSTERS")) m = std::min(m, atoi(getenv("B2O_FFT_CLUSTERS")));
+        ncl[dev & 63] = m > 0 ? m : -1;
+      }
+      if (!old_cols && ncl[dev & 63] > 0) {
+        if (colp::launch((float2 *)y, tw, s, ncl[dev & 63]) == cudaSuccess)
+          return cudaGetLastError() == cudaSuccess ? 0 : -1;
+        cudaGetLastError();
+        ncl[dev & 63] = -1;  // nothing ran: the cluster kernel below instead
+      }
       // cluster of 16 CTAs (non-portable size) when the device takes it, else 8 x 2 sub-FFTs
       static std::atomic<int> npc[64];
       if (npc[dev & 63] == 0 && getenv("B2O_FFT_NPC")) npc[dev & 63] = atoi(getenv("B2O_FFT_NPC"));
@@ -699,6 +927,7 @@ extern "C" void b2o_ops_warm(void) {
   cudaFuncGetAttributes(&a, fft16_cols_kernel);
   cudaFuncGetAttributes(&a, fft4k_rows_kernel);
   cudaFuncGetAttributes(&a, (const void *)fft4k_cols_cluster_kernel<1, 1>);
+  cudaFuncGetAttributes(&a, (const void *)colp::fft4k_cols_persist_kernel);
   cudaFuncGetAttributes(&a, (const void *)fft4k_cols_cluster_kernel<2, 1>);
   cudaGetLastError();
 }
