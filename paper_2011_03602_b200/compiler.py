@@ -42,13 +42,14 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-43"
+COMPILER_VERSION = "b2o-compiler-44"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
 # 258^3: 67.6 -> 53.4 us; tools/kernel_sweep.py, profiles/r01/README.md)
 MARCH_Z = 12  # planes per thread (NAS-MG resid 258^3, no prefetch: 8 -> 51.7 us, 16 -> 50.7 us; with the L2 prefetch 12 -> 41.9 us)
 MARCH_BLOCK = 128
+MARCH_SHFL = False     # plane-march: leading-plane +-1 chunks by warp shuffle (measured slower: 44.6 vs 39.0 us)
 MARCH_CHAINS = True    # plane-march: carry plane-local subexpressions as scalars (NAS-MG resid: 96 -> 72 registers, 41.9 -> 38.7 us)
 MARCH_FILL = True      # plane-march: carry chunks through unused middle planes (no reloads)
 MARCH_L2PF = 2         # plane-march L2 prefetch distance in planes (0: off; NAS-MG 258: 50.6 -> 42.7 us)
@@ -1701,8 +1702,22 @@ class _Gen:
             const = "const " if v not in n.writes else ""
             out.append(f"  {const}{self.T(v)} *__restrict__ v{v} = a.p{v};")
         out.extend(self._locals(n, "  "))
+        # warp-shuffle neighbour chunks (spec ``march_shfl``): the leading
+        # plane's chunks at quad offsets +-1 of a loaded chunk come from the
+        # neighbouring lane (same row: the lane's base address says so),
+        # halving the L1 wavefronts per step; every lane of the warp walks
+        # the same number of steps (predicated), so the shuffles converge
+        sh = bool(self.spec.get("march_shfl", MARCH_SHFL)) and not self.spec.get("march_async") and \
+            not self.spec.get("march_prefetch")
         out.append("  const uint32_t stride = gridDim.x * blockDim.x;")
-        out.append("  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {")
+        if sh:
+            out.append("  const uint32_t lane_ = threadIdx.x & 31u;")
+            out.append("  for (uint32_t tw_ = blockIdx.x * blockDim.x + threadIdx.x - lane_; tw_ < a.total; "
+                       "tw_ += stride) {")
+            out.append("    const uint32_t t = tw_ + lane_;")
+            out.append("    const bool act_ = t < a.total;")
+        else:
+            out.append("  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {")
         out.append("    if (t == a.total - 1u) {")
         out.extend(self._finals(n, "      "))
         out.append("    }")
@@ -1722,7 +1737,19 @@ class _Gen:
         out.append(f"    const int32_t k0_ = (int32_t)(b_ - F0_);")
         out.append(f"    const int32_t kr_ = k0_ - a.lo[{D - 1}];")
         out.append(f"    const int32_t kn_ = (int32_t)a.n[{D - 1}];")
-        out.append(f"    if (kr_ + {QUAD - 1} < 0 || kr_ >= kn_) continue;")
+        if sh:
+            out.append(f"    const bool ok_ = act_ && !(kr_ + {QUAD - 1} < 0 || kr_ >= kn_);")
+            out.append("    const uint32_t zw_ = __reduce_max_sync(0xffffffffu, ok_ ? zn_ : 0u);")
+            out.append("    const uint32_t bl_ = (uint32_t)b_;")
+            out.append("    const unsigned vm0_ = __ballot_sync(0xffffffffu, ok_);")
+            # neighbour lanes on the same row (their chunk is this chunk +-1)
+            for dl in (-1, 1):
+                nm = f"nb{'m' if dl < 0 else ''}{abs(dl)}_"
+                out.append(f"    const uint32_t {nm}b = __shfl_sync(0xffffffffu, bl_, (lane_ + ({dl})) & 31u);")
+                out.append(f"    const bool {nm} = (lane_ + ({dl})) < 32u && ((vm0_ >> ((lane_ + ({dl})) & 31u)) & 1u) "
+                           f"&& {nm}b == bl_ + {QUAD * dl}u;")
+        else:
+            out.append(f"    if (kr_ + {QUAD - 1} < 0 || kr_ >= kn_) continue;")
         C0 = mp["C0"]
         keys = set(mp["keys"])  # {(v, d, o)} chunks relative to the current plane
         ivs = set(qp["ivs"])
@@ -1835,7 +1862,11 @@ class _Gen:
 
         for v, d, o in sorted(keys):
             vt = "float4" if self.T(v) == "float" else "int4"
-            out.append(f"    {vt} {cname(v, d, o)} = {ldexpr(v, d, o)};")
+            if sh:
+                zero = "make_float4(0.f, 0.f, 0.f, 0.f)" if vt == "float4" else "make_int4(0, 0, 0, 0)"
+                out.append(f"    {vt} {cname(v, d, o)} = ok_ ? {ldexpr(v, d, o)} : {zero};")
+            else:
+                out.append(f"    {vt} {cname(v, d, o)} = {ldexpr(v, d, o)};")
 
         def dnm(d):
             return f"{'m' if d < 0 else ''}{abs(d)}"
@@ -1858,10 +1889,43 @@ class _Gen:
 
         for ch in (chains.values() if use_chains else ()):
             for d in range(ch["dmin"], ch["h"] + 1):
-                out.append(f"    {ch['T']} {ch['name']}{dnm(d)} = ({ch['T']})"
-                           f"{chain_expr(ch['e'], ch['u'], d, True)};")
+                val = f"({ch['T']}){chain_expr(ch['e'], ch['u'], d, True)}"
+                out.append(f"    {ch['T']} {ch['name']}{dnm(d)} = " + (f"ok_ ? {val} : ({ch['T']})0;" if sh else f"{val};"))
         carried = {k for k in keys if (k[0], k[1] + 1, k[2]) in keys and k[0] not in qp["writes"]}
         lead = sorted(keys - carried)
+        # shuffle sources: runs of consecutive leading chunks of one array and
+        # plane; the centre (most components used) is loaded, its +-1
+        # neighbours are shuffled from the adjacent lanes
+        sh_from: dict = {}
+        if sh:
+            used: dict = {}
+            for st in body:
+                for u in range(QUAD):
+                    stack = [st.value]
+                    while stack:
+                        e = stack.pop()
+                        if e[0] == "arr" and e[1] not in qp["writes"] and e[1] not in targets:
+                            d_, rest = mp["split"](affine(e[2], ivs)[1])
+                            used.setdefault((e[1], d_, (rest + u) // QUAD), set()).add((rest + u) % QUAD)
+                        elif e[0] == "bin":
+                            stack += [e[2], e[3]]
+            runs: list = []
+            for v, d, o in lead:
+                if v in qp["writes"]:
+                    continue
+                if runs and runs[-1][0] == (v, d) and runs[-1][-1] == o - 1:
+                    runs[-1].append(o)
+                else:
+                    runs.append([(v, d), o])
+            for run in runs:
+                (v, d), os_ = run[0], run[1:]
+                if len(os_) < 2:
+                    continue
+                mid = os_[len(os_) // 2]
+                oc = max(os_, key=lambda o: (len(used.get((v, d, o), ())), -abs(o - mid)))
+                for o in os_:
+                    if o != oc and abs(o - oc) == 1:
+                        sh_from[(v, d, o)] = oc
         # staged leading plane: each thread copies its own next-plane chunks
         # into private shared-memory slots (cp.async, P-stage ring) and reads
         # them back one step later -- no barrier (a thread reads only what it
@@ -1913,14 +1977,18 @@ class _Gen:
                 off = (dmax[v] + PF) * C0
                 pf_lines.append(f"{{ const char *pf_ = reinterpret_cast<const char *>(v{v} + b_ + {off}); "
                                 f"asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(pf_)); }}")
-            pf_guard = f"if (v{iv[0]} + {PF} < a.lo[0] + (int32_t)a.n[0])"
+            pf_guard = (f"if ({'live_ && ' if sh else ''}v{iv[0]} + {PF} < a.lo[0] + (int32_t)a.n[0])")
             for q in range(1, PF):  # prologue: the first steps' leading planes
-                out.append(f"    if (v{iv[0]} + {q} < a.lo[0] + (int32_t)a.n[0] && {q}u < zn_) {{")
+                out.append(f"    if ({'ok_ && ' if sh else ''}v{iv[0]} + {q} < a.lo[0] + (int32_t)a.n[0] && {q}u < zn_) {{")
                 for v in sorted(dmax):
                     out.append(f"      {{ const char *pf_ = reinterpret_cast<const char *>(v{v} + b_ + "
                                f"{(dmax[v] + q) * C0}); asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(pf_)); }}")
                 out.append("    }")
-        out.append("    for (uint32_t s_ = 0; s_ < zn_; ++s_) {")
+        if sh:
+            out.append("    for (uint32_t s_ = 0; s_ < zw_; ++s_) {")
+            out.append("      const bool live_ = ok_ && s_ < zn_;")
+        else:
+            out.append("    for (uint32_t s_ = 0; s_ < zn_; ++s_) {")
         out.append("      if (s_ > 0) {")
         out.append(f"        b_ += (int64_t){C0}; ++v{iv[0]};")
         for ch in (chains.values() if use_chains else ()):
@@ -1936,7 +2004,7 @@ class _Gen:
             out.append(f"        b2o_cp_wait<{P - 1}>();")
         # ascending plane offset: the old value of (d+1) is read before it
         # is replaced
-        for v, d, o in sorted(keys, key=lambda k: (k[1], k[0], k[2])):
+        for v, d, o in sorted(keys, key=lambda k: (k[1], k[0], (k in sh_from), k[2])):
             if (v, d, o) in carried:
                 out.append(f"        {cname(v, d, o)} = {cname(v, d + 1, o)};")
             elif staged and (v, d, o) in sidx:
@@ -1945,6 +2013,23 @@ class _Gen:
                            f"&st_[s_ % {P}u][{sidx[(v, d, o)]}][threadIdx.x]);")
             elif pipe:
                 out.append(f"        {cname(v, d, o)} = n{cname(v, d, o)};")
+            elif sh and (v, d, o) in sh_from:
+                oc = sh_from[(v, d, o)]
+                dl = o - oc
+                nm = f"nb{'m' if dl < 0 else ''}{abs(dl)}_"
+                vt = "float4" if self.T(v) == "float" else "int4"
+                T = self.T(v)
+                comps4 = []
+                for j in range(QUAD):
+                    x = f"{cname(v, d, o)}_{j}"
+                    out.append(f"        {T} {x} = __shfl_sync(0xffffffffu, {cname(v, d, oc)}.{'xyzw'[j]}, "
+                               f"(lane_ + ({dl})) & 31u);")
+                    comps4.append(x)
+                mk = "make_float4" if vt == "float4" else "make_int4"
+                out.append(f"        {cname(v, d, o)} = {mk}({', '.join(comps4)});")
+                out.append(f"        if (!{nm} && live_) {cname(v, d, o)} = {ldexpr(v, d, o)};")
+            elif sh:
+                out.append(f"        if (live_) {cname(v, d, o)} = {ldexpr(v, d, o)};")
             else:
                 out.append(f"        {cname(v, d, o)} = {ldexpr(v, d, o)};")
         for ch in (chains.values() if use_chains else ()):
@@ -1992,12 +2077,13 @@ class _Gen:
             v = st.target[1]
             c = qp["writes"][v]
             lanes = [f"r{si}_{u}" for u in range(QUAD)]
-            masked = [f"        if ((uint32_t)(kr_ + {u}) < (uint32_t)kn_) v{v}[b_ + ({c + u})] = r{si}_{u};"
+            live = "live_ && " if sh else ""
+            masked = [f"        if ({live}(uint32_t)(kr_ + {u}) < (uint32_t)kn_) v{v}[b_ + ({c + u})] = r{si}_{u};"
                       for u in range(QUAD)]
             if c % QUAD == 0:
                 vt = "float4" if self.T(v) == "float" else "int4"
                 mk = "make_float4" if vt == "float4" else "make_int4"
-                out.append(f"      if (kr_ >= 0 && kr_ + {QUAD} <= kn_) {{")
+                out.append(f"      if ({'live_ && ' if sh else ''}kr_ >= 0 && kr_ + {QUAD} <= kn_) {{")
                 out.append(f"        reinterpret_cast<{vt} *>(v{v} + b_)[{c // QUAD}] = {mk}({', '.join(lanes)});")
                 out.append("      } else {")
                 out.extend(masked)

@@ -36,6 +36,10 @@ OPTIONS = [
     {"flat_min_blocks": 2},
     {"march_tma": True, "quad_march": 32, "march_tma_stages": 4},
     {"march_tma": True},
+    {"march_shfl": True},
+    {"march_shfl": True, "quad_march": 5, "march_block": 64},
+    {"march_chains": False},
+    {"march_chains": False, "march_fill": False, "march_l2pf": 0},
 ]
 
 FUZZ = json.loads((GOLDEN / "fuzz.json").read_text())
