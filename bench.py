@@ -50,6 +50,11 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# torchrun sets OMP_NUM_THREADS=1 per rank; the CPU reference arm (rank 0
+# alone) and the N=1 cpu_baseline must use every host core they may, so the
+# OpenMP runtime is sized before anything loads it
+if "reference" in sys.argv or os.environ.get("WORLD_SIZE", "1") == "1":
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
 for p in (ROOT / "baseline" / "_ref",):
     if p.exists():
         sys.path.append(str(p))
