@@ -42,7 +42,7 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-44"
+COMPILER_VERSION = "b2o-compiler-45"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
@@ -2117,6 +2117,11 @@ class _Gen:
         R, TI, TJ, BK = int(self.spec.get("ktile_r", KT_R)), T, T, KT_BK
         RI = int(self.spec.get("ktile_ri", R))  # micro-tile rows (i); R columns (j)
         nthr = TI * TJ // (RI * R)
+        if TI % RI or TJ % R or (BK * TI) % nthr or (BK * TJ) % nthr or nthr % 32 or nthr > 1024:
+            # the staging loops move BK * T / nthr elements per thread: a tile
+            # that does not divide evenly would leave operands unstaged
+            raise CompileError(f"k-tile shape {TI} x {TJ} with {RI} x {R} micro-tiles is unsupported: "
+                               f"{nthr} threads must be a multiple of 32 dividing {BK} x the tile edge")
         TX = TJ // R  # threads along j
         K = prog.loops[kp["kloop"]]
         body = prog.regions[prog.loops[n.chain[1]].body].statements

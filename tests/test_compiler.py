@@ -131,3 +131,17 @@ def test_ktile_staging_covers_each_tile_element_once(opts):
                 for w in range(nthr // 32):
                     banks = {(_c_int(kk, tid) * pitch + _c_int(oo, tid)) % 32 for tid in range(32 * w, 32 * w + 32)}
                     assert len(banks) == 32, (kk, oo, w, len(banks))
+
+
+def test_ktile_shape_that_cannot_stage_is_rejected():
+    """A k-tile edge whose staging does not divide evenly over the threads
+    (60 x 60 tiles: 225 threads) would leave operands unstaged; the compiler
+    refuses it instead of producing wrong sums."""
+    import pytest as _pt
+
+    from paper_2011_03602_b200.compiler import CompileError, generate_sources
+
+    g = golden("matmul_48")
+    with _pt.raises(CompileError, match="k-tile shape"):
+        generate_sources(g["doc"], dict(g["spec"], ktile_tile=60))
+    generate_sources(g["doc"], dict(g["spec"], ktile_tile=32))  # supported shapes still build
