@@ -657,6 +657,8 @@ def ga_arm(args, dist: Dist) -> dict | None:
            "dedupe": ("genomes whose GPU roots and transfer plan coincide share one program run "
                       "(B200Evaluator.run_key, SURVEY.md §8e)") if args.ga_dedupe else "off",
            "history_evals": [h.evaluations for h in res.history][:6]}
+    if dist.world == 1 and args.ga_workers > 1:
+        out["overlapped"] = _guarded(ga_overlapped, args, g, model, params, out["best_genome"])
     if dist.rank == 0:
         t0 = time.perf_counter()
         ref = run_search(model, screen_model(model), CostModelEvaluator(), params)
@@ -667,6 +669,36 @@ def ga_arm(args, dist: Dist) -> dict | None:
             "cores": 1, "what": "reference run_search + CostModelEvaluator (synthetic cost, no program executed), "
                                 "same model/params; the fitness the reference ships with"}
     return out
+
+
+def ga_overlapped(args, g: dict, model, params, best_solo: str) -> dict:
+    """The same GA with W workers sharing the one B200 (host loops of one
+    pattern overlap the GPU work of another; the runtime in a child process,
+    isolated.IsolatedEvaluator), and the k fastest genomes re-measured alone
+    at the end (run_search_batched confirm_top) because concurrent patterns
+    drift (tools/ga_drift.py).  Not the headline GA: a throughput option."""
+    from gpuoffload.screen import screen_model
+
+    from paper_2011_03602_b200.isolated import IsolatedEvaluator
+    from paper_2011_03602_b200.search import run_search_batched
+
+    W = int(args.ga_workers)
+    ev = IsolatedEvaluator(g["spec"], devices=[0] * W, timeout_seconds=args.ga_timeout, dedupe=bool(args.ga_dedupe))
+    try:
+        first = sorted(g["patterns"])[0]
+        ev.measure_payloads(g["doc"], [g["patterns"][first]])  # child up, program loaded, reference run (untimed)
+        stats: dict = {}
+        t0 = time.perf_counter()
+        res = run_search_batched(model, screen_model(model), ev, params, stats=stats, confirm_top=3, confirm_repeats=2)
+        wall = time.perf_counter() - t0
+    finally:
+        ev.close()
+    best = "".join(map(str, res.best_genome))
+    return {"workers_per_gpu": W, "patterns_per_s": round(res.evaluations_performed / wall, 3),
+            "evaluations": res.evaluations_performed, "wall_s": round(wall, 3), "best_genome": best,
+            "best_time_s": res.best_time, "same_winner_as_one_worker": best == best_solo,
+            "confirmed_top3": stats.get("confirmed"), "programs_executed": ev.programs_executed,
+            "note": "wall includes the solo re-measurement of the 3 fastest genomes"}
 
 
 def ops_arm(dist: Dist) -> dict:
@@ -768,6 +800,8 @@ def main() -> None:
     ap.add_argument("--ga-seed", type=int, default=20201106)
     ap.add_argument("--ga-timeout", type=float, default=120.0)
     ap.add_argument("--ga-dedupe", type=int, default=1, help="run identical programs (same GPU roots + plan) once")
+    ap.add_argument("--ga-workers", type=int, default=2,
+                    help="also run the GA with this many workers sharing the B200 (N=1 only; 1 = skip)")
     args = ap.parse_args()
     dist = Dist()
     try:
