@@ -696,7 +696,9 @@ def ga_overlapped(args, g: dict, model, params, best_solo: str) -> dict:
     best = "".join(map(str, res.best_genome))
     return {"workers_per_gpu": W, "patterns_per_s": round(res.evaluations_performed / wall, 3),
             "evaluations": res.evaluations_performed, "wall_s": round(wall, 3), "best_genome": best,
-            "best_time_s": res.best_time, "same_winner_as_one_worker": best == best_solo,
+            "best_time_s": res.best_time,
+            "same_program_as_one_worker": IsolatedEvaluator.run_key("", g["patterns"][best])
+            == IsolatedEvaluator.run_key("", g["patterns"][best_solo]),
             "confirmed_top3": stats.get("confirmed"), "programs_executed": ev.programs_executed,
             "note": "wall includes the solo re-measurement of the 3 fastest genomes"}
 

@@ -70,6 +70,7 @@ class IsolatedEvaluator:
     evaluator_id = EVALUATOR_ID
     concurrency_safe = True
     needs_code = False
+    run_key = staticmethod(B200Evaluator.run_key)
 
     def __init__(self, app_spec: dict, devices: list[int] | None = None, mode: str = "coherent",
                  timeout_seconds: float = 300.0, repeats: int = 1, reference_outputs: dict | None = None,

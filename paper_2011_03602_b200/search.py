@@ -206,13 +206,26 @@ def run_search_batched(model, verdicts, evaluator, params, backend: str = "c_ope
 
 
 def _confirm(runner, k: int, repeats: int, best_bits, best_time, stats):
-    """Re-measure the k fastest feasible genomes alone (see
-    ``run_search_batched``); ties keep the search's order."""
-    ranked = sorted((f.time, bits) for bits, f in runner.cache.items() if f.time is not None)[:k]
+    """Re-measure the k fastest feasible programs alone (see
+    ``run_search_batched``).  Genomes that run the identical program (same
+    GPU roots and plan: ``B200Evaluator.run_key``) are one candidate,
+    represented by its first genome in the search's order, so measurement
+    noise cannot pick between copies of one program; ties keep that order."""
+    ranked = sorted((f.time, bits) for bits, f in runner.cache.items() if f.time is not None)
     solo = getattr(runner.evaluator, "measure_solo", None)
-    rows = []
+    run_key = getattr(runner.evaluator, "run_key", None)
+    rows, seen = [], set()
     for t_search, bits in ranked:
+        if len(rows) == k:
+            break
         req = runner._request(bits, {"confirm": True})
+        if run_key is not None:
+            from .evaluator import payload_from_request
+
+            key = run_key("", payload_from_request(req))
+            if key in seen:
+                continue
+            seen.add(key)
         res = solo(req, repeats) if solo is not None else runner._measure_one(req)
         rows.append((bits, t_search, res.time_seconds))
     if stats is not None:
