@@ -802,7 +802,7 @@ def main() -> None:
     ap.add_argument("--ga-seed", type=int, default=20201106)
     ap.add_argument("--ga-timeout", type=float, default=120.0)
     ap.add_argument("--ga-dedupe", type=int, default=1, help="run identical programs (same GPU roots + plan) once")
-    ap.add_argument("--ga-workers", type=int, default=2,
+    ap.add_argument("--ga-workers", type=int, default=4,
                     help="also run the GA with this many workers sharing the B200 (N=1 only; 1 = skip)")
     args = ap.parse_args()
     dist = Dist()
