@@ -394,6 +394,9 @@ void ensure_host(AppDev *d, int v, bool async_ok = false) {
   }
   if (d->mode == B2O_MODE_LITERAL) {
     d->acc.stale_reads++;
+    // the program reads its host copy as the plan left it: pristine unless
+    // this job changed it -- what an eager reset would have shown
+    host_fresh(d, v);
     return;
   }
   copy_d2h(d, v, async_ok);

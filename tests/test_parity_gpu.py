@@ -118,6 +118,45 @@ def test_literal_equals_coherent_when_plan_is_complete(evaluators):
         assert r["validity"] == "valid" and r["stale_reads"] == 0, (x, r)
 
 
+@pytest.mark.parametrize("mode", ["coherent", "literal"])
+def test_job_results_do_not_depend_on_the_previous_job(evaluators, mode):
+    """The reset between jobs restores host copies lazily (b2o_runtime.cu
+    reset_state / host_fresh): a job's verdict, comparison and final state
+    must not depend on which pattern ran before it on the same replica, in
+    either mode.  12 Himeno XS genomes, each on a fresh replica, then all of
+    them forward and backward on one replica."""
+    from paper_2011_03602_b200.ir import Program
+
+    g = golden("himeno_xs_inline")
+    pats = g["patterns"]
+    order = sorted(pats)[::5][:12]
+    prog = Program(g["doc"])
+    outs = [prog.var_by_name[o].id for o in g["spec"]["outputs"]]
+    fresh = {}
+    for x in order:
+        ev = evaluators(f"order_{mode}_{x}", g["spec"], mode=mode)
+        r = ev.measure_payloads(g["doc"], [pats[x]])[0]
+        fresh[x] = (r, [ev.app_for(g["doc"]).read(v, worker=r["worker"]).tobytes() for v in outs])
+    ev = evaluators(f"order_{mode}_chain", g["spec"], mode=mode)
+    app = ev.app_for(g["doc"])
+    for x in order + order[::-1]:
+        r = ev.measure_payloads(g["doc"], [pats[x]])[0]
+        f, fstate = fresh[x]
+        assert (r["validity"], r["mismatches"], r["max_rel_err"], r["stale_reads"]) == \
+            (f["validity"], f["mismatches"], f["max_rel_err"], f["stale_reads"]), (mode, x, r, f)
+        assert [app.read(v, worker=r["worker"]).tobytes() for v in outs] == fstate, (mode, x)
+
+
+def test_literal_noread_repeats_identically(evaluators):
+    """The literal no-read genome reads a host copy of p that the coherent
+    path would have refreshed: run after run on one replica it must see the
+    same (pristine) bytes, whatever the previous run left there."""
+    g = golden("himeno_xs_noread")
+    ev = evaluators("noread_literal_repeat", g["spec"], mode="literal")
+    rs = [ev.measure_payloads(g["doc"], [g["patterns"]["100100"]])[0] for _ in range(3)]
+    assert len({(r["validity"], r["mismatches"], r["max_rel_err"], r["stale_reads"]) for r in rs}) == 1, rs
+
+
 def test_hoisted_plan_moves_fewer_bytes_than_unhoisted(evaluators):
     """The hoisting rule (src/transfers.py:120-191) realised on the device:
     the four_loops genome-101 plan executes fewer directive instances."""
