@@ -200,7 +200,7 @@ int launch_hist(const int32_t *d, int64_t n, T *h, int64_t bins, cudaStream_t s)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t smem_cap = 96 * 1024;  // two CTAs per SM
+  const int64_t smem_cap = 96 * 1024;  // at least two CTAs per SM
   if (bins * 4 <= smem_cap) {
     const int warps = kHistThreads / 32;
     int copies = (int)std::min<int64_t>(warps, smem_cap / (bins * 4));
@@ -208,7 +208,11 @@ int launch_hist(const int32_t *d, int64_t n, T *h, int64_t bins, cudaStream_t s)
     const size_t smem = (size_t)copies * bins * 4;
     cudaFuncSetAttribute(hist_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap);
     const int64_t want = (n / 4 + kHistThreads - 1) / kHistThreads;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 2));
+    // three CTAs per SM when their private copies fit (64 M int32, 256 bins:
+    // 48.1 -> 44.0 us, 0.85 -> 0.93 of HBM; four: 44.6 us)
+    static const int env_per_sm = getenv("B2O_HIST_CTAS") ? atoi(getenv("B2O_HIST_CTAS")) : 0;
+    const int per_sm = env_per_sm > 0 ? env_per_sm : (smem <= 72 * 1024 ? 3 : 2);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
     hist_smem_kernel<T><<<grid, kHistThreads, smem, s>>>(d, n, h, (int)bins, copies);
   } else {
     const int64_t want = (n + kHistThreads - 1) / kHistThreads;
