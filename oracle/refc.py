@@ -440,7 +440,7 @@ def golden_programs(golden_dir: Path) -> list[tuple[dict, str]]:
     fuzz = json.loads((golden_dir / "fuzz.json").read_text())
     items += [(fuzz[k]["doc"], "fp64") for k in sorted(fuzz, key=int)[:16]]
     for a in ("four_loops", "nest2d", "stencil", "triple_nest", "himeno_xs_inline", "himeno_17x9x33", "matmul_48",
-              "nasmg_18"):
+              "nasmg_18", "himeno_M"):
         items.append((json.loads((golden_dir / f"{a}.json").read_text())["doc"], "fp64"))
     return items
 

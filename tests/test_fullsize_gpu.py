@@ -50,6 +50,38 @@ def test_himeno_M_every_program():
     assert res["010010"]["launches"] == 20 * 2 * 127  # j-roots: one launch per host i iteration
 
 
+def test_himeno_M_fp64_every_program():
+    """The north star's fp64 class at a BASELINE size: Himeno M compiled with
+    ``precision: fp64`` (C double: flat kernels, 8-byte transfers), every
+    distinct program byte-equal to the reference's emission compiled
+    ``-Dfloat=double``."""
+    import copy
+
+    from paper_2011_03602_b200.evaluator import B200Evaluator
+    from paper_2011_03602_b200.ir import Program
+
+    g = copy.deepcopy(golden("himeno_M"))
+    g["spec"]["precision"] = "fp64"
+    prog = Program(g["doc"])
+    want = oracle_final(g["doc"], g["spec"])
+    ev = B200Evaluator(g["spec"], devices=[0])
+    app = ev.app_for(g["doc"])
+    seen = set()
+    for x in sorted(g["patterns"]):
+        key = B200Evaluator.run_key("", g["patterns"][x])
+        if key in seen:
+            continue
+        seen.add(key)
+        r = ev.measure_payloads(g["doc"], [g["patterns"][x]])[0]
+        assert r["validity"] == "valid", (x, r["diag"])
+        for o in g["spec"]["outputs"]:
+            vid = prog.var_by_name[o].id
+            got = app.read(vid, worker=r["worker"])
+            assert got.dtype.itemsize == 8 or prog.vars[vid].base_type == "int"
+            assert got.tobytes() == np.asarray(want[vid], dtype=got.dtype).tobytes(), (x, o)
+    assert len(seen) == 16
+
+
 def test_himeno_L_every_program():
     """Config 5's GA workload (257x257x513): the 16 programs the GA measures."""
     res = _check("himeno_L")
