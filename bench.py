@@ -696,9 +696,12 @@ def ga_overlapped(args, g: dict, model, params, best_solo: str) -> dict:
     best = "".join(map(str, res.best_genome))
     return {"workers_per_gpu": W, "patterns_per_s": round(res.evaluations_performed / wall, 3),
             "evaluations": res.evaluations_performed, "wall_s": round(wall, 3), "best_genome": best,
-            "best_time_s": res.best_time,
+            "best_time_s": res.best_time, "one_worker_best_genome": best_solo,
             "same_program_as_one_worker": IsolatedEvaluator.run_key("", g["patterns"][best])
             == IsolatedEvaluator.run_key("", g["patterns"][best_solo]),
+            "noise_note": "Himeno L's two fastest programs (100100, 100010) are ~1 % apart: single measurements "
+                          "(the reference GA's one per genome) swap them from run to run; the confirmation times "
+                          "the top 3 alone, best of 2",
             "confirmed_top3": stats.get("confirmed"), "programs_executed": ev.programs_executed,
             "note": "wall includes the solo re-measurement of the 3 fastest genomes"}
 
