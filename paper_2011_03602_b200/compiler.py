@@ -42,13 +42,14 @@ from .ir import Program, expr_vars
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 CACHE = Path(os.environ.get("B2O_CACHE", PKG / "_cache"))
-COMPILER_VERSION = "b2o-compiler-45"
+COMPILER_VERSION = "b2o-compiler-47"
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BLOCK_THREADS = 256
 # plane-marching quad kernel: planes per thread and CTA size (NAS-MG resid
 # 258^3: 67.6 -> 53.4 us; tools/kernel_sweep.py, profiles/r01/README.md)
 MARCH_Z = 12  # planes per thread (NAS-MG resid 258^3, no prefetch: 8 -> 51.7 us, 16 -> 50.7 us; with the L2 prefetch 12 -> 41.9 us)
 MARCH_BLOCK = 128
+QUAD_NEXTPF = True     # quad kernels launched per host iteration prefetch the next launch's chunks (Himeno L 001001: 1.57 -> 1.28 s)
 MARCH_SHFL = False     # plane-march: leading-plane +-1 chunks by warp shuffle (measured slower: 44.6 vs 39.0 us)
 MARCH_CHAINS = True    # plane-march: carry plane-local subexpressions as scalars (NAS-MG resid: 96 -> 72 registers, 41.9 -> 38.7 us)
 MARCH_FILL = True      # plane-march: carry chunks through unused middle planes (no reloads)
@@ -966,6 +967,27 @@ class _Gen:
 
     # -- kernels -------------------------------------------------------------------
 
+    def next_pf(self, n: NestPlan):
+        """(host loop, element stride) when a plain quad kernel is launched
+        once per iteration of an enclosing host loop whose index enters its
+        addresses (k-rooted Himeno: one launch per (i, j), stride = the row
+        pitch): the kernel then prefetches into L2 what the NEXT launch will
+        read -- its own chunks shifted by one host iteration -- so that launch
+        finds its rows in L2 instead of paying DRAM latency (spec
+        ``quad_nextpf``).  The launch stub passes whether that iteration
+        exists, so every prefetched address is one the program reads."""
+        if n.shape != "quad" or n.quad.get("march") or not self.spec.get("quad_nextpf", QUAD_NEXTPF):
+            return None
+        par = self.prog.loops[n.root].parent
+        if par is None:
+            return None
+        pv = self.prog.loops[par].index_var
+        qp = n.quad
+        if pv not in qp["ovars"]:
+            return None
+        c = qp["outer"][qp["ovars"].index(pv)]
+        return (par, c) if c else None
+
     def kernel_struct(self, n: NestPlan) -> list[str]:
         D = max(len(n.chain), 1)
         out = [f"typedef struct {{", "  uint32_t total, chunk;",
@@ -978,6 +1000,8 @@ class _Gen:
             out.append(f"  {self.T(v)} s{v};")
         for v in (n.exact or {}):
             out.append(f"  {self.T(v)} *xb{v};  // per-point terms of reduction {self.prog.vars[v].name}, loop order")
+        if self.next_pf(n):
+            out.append("  int32_t pfn;  // the enclosing host loop has a next iteration")
         out.append(f"}} KA_L{n.root};")
         return out
 
@@ -1018,6 +1042,11 @@ class _Gen:
             for d in range(1, len(n.chain)):
                 out.append(f"  b2o_fastdiv_init(a.tn[{d}], &a.mul[{d}], &a.shr[{d}]);")
         out.append("  a.total = (uint32_t)total; a.slab = ex->slab; a.scratch = ex->scratch;")
+        npf = self.next_pf(n)
+        if npf:
+            par = prog.loops[npf[0]]
+            out.append(f"  a.pfn = ({self.host_name(par.index_var, False)} + 1 < "
+                       f"{self.bound(par.upper, self.host_name)}) ? 1 : 0;")
         for v in n.arrays:
             const = "const " if v not in n.writes else ""
             out.append(f"  a.p{v} = ({const}{self.T(v)} *)ex->dev[{v}];")
@@ -1326,6 +1355,15 @@ class _Gen:
                 return f"(reinterpret_cast<const {vt} *>(v{v} + b_)[{o}])"
             return f"__ldg(reinterpret_cast<const {vt} *>(v{v} + b_) + ({o}))"
 
+        npf = self.next_pf(n)
+        if npf and not shfl:
+            # the next launch's chunks (one host iteration further): L2 prefetch
+            ro = sorted({(v, o) for v, o in chunks if v not in qp["writes"]})
+            out.append("    if (a.pfn) {")
+            for v, o in ro:
+                out.append(f"      {{ const char *pf_ = reinterpret_cast<const char *>(v{v} + b_ + {npf[1]} + "
+                           f"{QUAD * o}); asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(pf_)); }}")
+            out.append("    }")
         shuffled: set = set()  # chunks held as per-lane scalars taken from neighbours
         if not shfl:
             for v, o in chunks:

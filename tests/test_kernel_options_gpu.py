@@ -40,6 +40,7 @@ OPTIONS = [
     {"march_shfl": True, "quad_march": 5, "march_block": 64},
     {"march_chains": False},
     {"march_chains": False, "march_fill": False, "march_l2pf": 0},
+    {"quad_nextpf": False},
 ]
 
 FUZZ = json.loads((GOLDEN / "fuzz.json").read_text())
