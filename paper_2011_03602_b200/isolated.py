@@ -29,7 +29,6 @@ same isolation without paying a process per pattern:
 from __future__ import annotations
 
 import multiprocessing as mp
-import time
 
 from .evaluator import EVALUATOR_ID, B200Evaluator, _result_cls, payload_from_request
 from .ir import document_digest, document_of
@@ -246,12 +245,3 @@ class IsolatedEvaluator:
         r["solo"] = True
         self.log.append(r)
         return self._result(r)
-
-
-def wait_ready(ev: IsolatedEvaluator, timeout: float = 600.0) -> bool:
-    """Start the child and wait until its runtime is up (tests, benches)."""
-    t0 = time.time()
-    while time.time() - t0 < timeout:
-        if ev.parallel_width >= 1:
-            return True
-    return False
