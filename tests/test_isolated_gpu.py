@@ -70,3 +70,33 @@ def test_plugin_protocol_through_child(iso):
     out = ev.measure_batch(reqs)
     assert len(out) == 8 and all(r.validity == "valid" and r.time_seconds > 0 for r in out)
     assert ev.parallel_width == 1
+
+
+@pytest.mark.skipif(not has_reference(), reason="reference not importable")
+def test_two_workers_ga_with_confirmation():
+    """The throughput mode: the reference GA over two workers sharing the
+    B200 in an isolated child, the fastest programs re-measured alone; the
+    result is a valid genome whose confirmed time is a solo measurement."""
+    import json
+
+    from gpuoffload.ga import GAParams
+    from gpuoffload.irdoc import load_ir_document
+    from gpuoffload.screen import screen_model
+
+    from paper_2011_03602_b200.isolated import IsolatedEvaluator
+    from paper_2011_03602_b200.search import run_search_batched
+
+    g = golden("himeno_17x9x33")
+    model = load_ir_document(json.dumps(g["doc"]))
+    ev = IsolatedEvaluator(g["spec"], devices=[0, 0], timeout_seconds=60)
+    try:
+        assert ev.parallel_width == 2
+        stats = {}
+        res = run_search_batched(model, screen_model(model), ev, GAParams(population_size=16, generations=4, seed=3),
+                                 stats=stats, confirm_top=2, confirm_repeats=2)
+    finally:
+        ev.close()
+    assert res.best_time is not None and res.best_time > 0
+    rows = stats["confirmed"]
+    assert 1 <= len(rows) <= 2 and all(s is not None for _, _, s in rows)
+    assert res.best_time == min(s for _, _, s in rows)
